@@ -1,0 +1,431 @@
+"""Benchmark: batched Jacobi-Richardson(32) sweeps on 1023^2 anisotropic grids.
+
+Workload (BASELINE.json configs[2], the north-star "batched N=1023
+Richardson(m) stencil sweeps"; SURVEY.md §8(d) cfg 3): 8 independent
+anisotropic systems per GPU on 1024x1024 cells (1023^2 unknowns, f64),
+theta ~ U[0, pi], lg eps ~ U[-4, 0], f ~ N(0,1) (rng = default_rng(3), drawn
+per system in that order), weighted Jacobi (relax 2/3), m = 32 Chebyshev
+weights of the Jacobi-scaled operator in Leja order.  Synthetic seeded
+inputs: the reference has no dataset.
+
+One step = one outer sweep (32 inner updates) over all systems of a GPU.
+  value     grid-point updates/s, whole job (all ranks), iterates resident in HBM
+  e2e       same metric through the public API (solve_stationary_batched) with
+            pinned host buffers: H2D of f and u0, D2H of u inside the timing
+  roofline  dominant kernel (temporally blocked sweep): algorithmic bytes per
+            launch (24 B per point-update) / CUDA-event time
+  time_to_tol  wall time of the full solve of the batch to ||r||/||f|| < 1e-6
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import os
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+os.environ.setdefault("MKL_NUM_THREADS", "1")
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+from pathlib import Path  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "grid-point updates/s + time-to-1e-6 residual (1 B200, % HBM roofline) vs CPU ref"
+UNIT = "grid-point updates/s"
+N_SIDE = 1024            # cells per side -> 1023^2 unknowns
+SYSTEMS_PER_GPU = 8
+M = 32
+BYTES_PER_UPDATE = 24    # plain Richardson f64: read u, f; write u
+TOL = 1e-6
+MAX_OUTER_TOL = 10_000
+
+
+# ------------------------------------------------------------------ inputs
+def draw_systems(first, count, n=N_SIDE, seed=3):
+    """(eps, theta, f) for systems first..first+count-1 of the global stream."""
+    rng = np.random.default_rng(seed)
+    out = []
+    P = (n - 1) ** 2
+    for b in range(first + count):
+        theta = rng.uniform(0.0, np.pi)
+        eps = 10.0 ** rng.uniform(-4.0, 0.0)
+        f = rng.standard_normal(P)
+        if b >= first:
+            out.append((float(eps), float(theta), f))
+    return out
+
+
+def schedule_for(eps, theta, n=N_SIDE):
+    """Jacobi scale and the Leja-ordered Chebyshev weights of the scaled operator."""
+    from paper_2412_08076_b200.problems import AnisotropicProblem, anisotropic_stencil
+    from paper_2412_08076_b200.schedules import chebyshev_weights, leja_order, stencil_symbol_bounds
+    c = anisotropic_stencil(AnisotropicProblem(eps, theta, n))
+    scale = (2.0 / 3.0) / c[4]          # precond.py:71-77, relax / diag
+    lmax, lmin = stencil_symbol_bounds(c, n)
+    w = leja_order(chebyshev_weights(scale * lmax, scale * lmin, M))
+    return c, scale, w
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU side
+def _cpu_worker_init(eps, theta, n, seed_f):
+    global _W
+    import oracle as O
+    A = O.assemble_anisotropic(eps, theta, n)
+    f = np.random.default_rng(seed_f).standard_normal(A.shape[0])
+    u = np.zeros(A.shape[0])
+    _W = dict(A=A, f=f, u=u, r=f - A.dot(u), scale=O.jacobi_scale(A),
+              w=schedule_for(eps, theta, n)[2], i=0)
+
+
+def _cpu_worker_steps(k):
+    """k inner steps of Jacobi Richardson on this worker's system (the
+    oracle's restatement of richardson.py:111-125, same SciPy/NumPy calls)."""
+    A, f, sc, w = _W["A"], _W["f"], _W["scale"], _W["w"]
+    u, r, i0 = _W["u"], _W["r"], _W["i"]
+    t0 = time.perf_counter()
+    for i in range(i0, i0 + k):
+        v = w[i % M] * (sc * r)
+        u = u + v
+        r = f - A.dot(u)
+        float(np.linalg.norm(r))
+    _W.update(u=u, r=r, i=i0 + k)
+    return time.perf_counter() - t0
+
+
+class CpuReference:
+    """The oracle port of the reference path on all host cores: one process
+    per system (OPENBLAS_NUM_THREADS=1, as SURVEY.md §8(d) prescribes)."""
+
+    def __init__(self, workers=None, n=N_SIDE):
+        import multiprocessing as mp
+        self.cores = workers or min(32, len(os.sched_getaffinity(0)))
+        systems = draw_systems(0, min(self.cores, SYSTEMS_PER_GPU), n)
+        ctx = mp.get_context("fork")
+        self.pools = []
+        for k in range(self.cores):
+            eps, th, _ = systems[k % len(systems)]
+            self.pools.append(ctx.Pool(1, initializer=_cpu_worker_init, initargs=(eps, th, n, 100 + k)))
+        self.n = n
+        for p in self.pools:   # wait for assembly
+            p.apply(_cpu_worker_steps, (0,))
+
+    def run(self, k):
+        """Wall time for every worker to run k inner steps concurrently."""
+        t0 = time.perf_counter()
+        res = [p.apply_async(_cpu_worker_steps, (k,)) for p in self.pools]
+        for r in res:
+            r.get()
+        return time.perf_counter() - t0
+
+    def updates(self, k):
+        return self.cores * (self.n - 1) ** 2 * k
+
+    def close(self):
+        for p in self.pools:
+            p.terminate()
+
+
+# ------------------------------------------------------------------ dist
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return rank, world, local
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ arms
+def config_dict(block_T):
+    return {"workload": "cfg3: 8 anisotropic systems/GPU on 1024^2 cells (1023^2 unknowns), "
+                        "weighted-Jacobi Richardson(32), Leja-ordered Chebyshev weights, f64",
+            "systems_per_gpu": SYSTEMS_PER_GPU, "grid": N_SIDE - 1, "m": M,
+            "step": "one outer sweep (32 inner updates) of every system",
+            "block_T": block_T, "l2": "no flush: per-GPU working set 3 x 67 MB > 126 MB L2",
+            "seed": 3}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU port of the reference path, rank 0 only."""
+    if rank != 0:
+        return None
+    ref = CpuReference()
+    k_inner = 2   # inner steps per worker per step (bounded sample)
+    for _ in range(args.warmup):
+        ref.run(k_inner)
+    times = [ref.run(k_inner) for _ in range(args.steps)]
+    ref.close()
+    t = float(np.sum(times))
+    upd = ref.updates(k_inner) * args.steps
+    value = upd / t
+    sample = (f"{ref.cores} processes x 1 system (1023^2) x {k_inner} Jacobi-Richardson inner "
+              f"steps per step, oracle port (SciPy CSR matvec + NumPy), OPENBLAS_NUM_THREADS=1")
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(None), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def run_gpu(args, rank, world, local):
+    import torch
+    import paper_2412_08076_b200 as G
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    systems = draw_systems(rank * SYSTEMS_PER_GPU, SYSTEMS_PER_GPU)
+    probs, scheds, scales = [], [], []
+    for eps, th, _ in systems:
+        c, sc, w = schedule_for(eps, th)
+        probs.append(G.AnisotropicProblem(eps, th, N_SIDE))
+        scheds.append(G.WeightSchedule(omega=w))
+        scales.append(sc)
+    op = G.GpuStencilOperator.from_problems(probs, dtype=np.float64, device=dev)
+    F = np.stack([f for _, _, f in systems])
+    P = [G.JacobiScale(np.float64(s)) for s in scales]
+    B, Pn = op.batch, op.P
+
+    # ---- device-resident timed sweeps
+    S = G.StationarySolver(op, scheds, P, tol=1e-300, max_outer=10**7, block_T=args.block_T)
+    S.begin(F)
+    stream = torch.cuda.current_stream()
+    launches_per_step = None
+    for _ in range(args.warmup):
+        n0 = S.info()[2]
+        steps = 0
+        while steps < M:
+            steps += S.step()
+        launches_per_step = S.info()[2] - n0
+    torch.cuda.synchronize()
+    block_T = S.info()[1]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps * launches_per_step)]
+    k_launch = [0] * len(ev)
+    barrier(world)
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        e = 0
+        for _ in range(args.steps):
+            steps = 0
+            while steps < M:
+                ev[e][0].record(stream)
+                k_launch[e] = S.step()
+                ev[e][1].record(stream)
+                steps += k_launch[e]
+                e += 1
+        stop.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    t_local = start.elapsed_time(stop) / 1e3
+    t = max_over_ranks(t_local, world)
+    upd_step = B * Pn * M
+    value = world * upd_step * args.steps / t
+    # dominant kernel: the full-depth blocked launches
+    full = [i for i in range(e) if k_launch[i] == block_T]
+    dur = np.array([ev[i][0].elapsed_time(ev[i][1]) / 1e3 for i in full])
+    avg = float(dur.mean())
+    alg_bytes = BYTES_PER_UPDATE * B * Pn * block_T
+    achieved = alg_bytes / avg / 1e9
+    peak = _peak_hbm()
+    share = float(dur.sum() / t_local)
+
+    # ---- end to end through the public API, pinned host buffers
+    Fh = torch.from_numpy(F).pin_memory()
+    Uh = torch.zeros_like(Fh).pin_memory()
+    e2e_times = []
+    for it in range(args.warmup + args.e2e_steps):
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        res = G.solve_stationary_batched(op, Fh, scheds, P, tol=1e-300, max_outer=1, u0=Uh)
+        U = np.stack([u for u, _ in res])
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        Uh.copy_(torch.from_numpy(U))
+        if it >= args.warmup:
+            e2e_times.append(max_over_ranks(dt, world))
+    e2e_value = world * upd_step / float(np.mean(e2e_times))
+
+    # ---- time to 1e-6 for the whole batch
+    ttt = None
+    if args.time_to_tol:
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        S2 = G.StationarySolver(op, scheds, P, tol=TOL, max_outer=MAX_OUTER_TOL, block_T=args.block_T)
+        S2.begin(F)
+        S2.run(first_batch=16, max_batch=256)
+        torch.cuda.synchronize()
+        dt = max_over_ranks(time.perf_counter() - t0, world)
+        reps = [S2.report(b)[0] for b in range(B)]
+        ttt = {"seconds": dt, "tol": TOL, "max_outer": MAX_OUTER_TOL,
+               "converged": [int(r.status == 1) for r in reps],
+               "outer_sweeps": [int(r.iterations) for r in reps],
+               "inner_iterations": [int(r.inner_iterations) for r in reps],
+               "final_rel": [float(r.final_relative_residual) for r in reps]}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu:
+            ref = CpuReference()
+            k_inner = 16
+            tc = ref.run(k_inner)
+            cpu = {"value": ref.updates(k_inner) / tc, "unit": UNIT, "cores": ref.cores,
+                   "kind": "port",
+                   "sample": f"{ref.cores} processes x 1 system (1023^2) x {k_inner} inner steps "
+                             f"of the oracle port, {tc:.1f} s wall"}
+            ref.close()
+        traffic = _ncu_traffic(block_T)
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic", "config": config_dict(block_T),
+               "clocks": clk.summary(),
+               "e2e": {"value": e2e_value, "unit": UNIT,
+                       "h2d_bytes_per_step": int(2 * F.nbytes), "d2h_bytes_per_step": int(F.nbytes),
+                       "api": "solve_stationary_batched(op, f_pinned, schedules, P, max_outer=1, "
+                              "u0=u_pinned)"},
+               "gpu_launches": int(e),
+               "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak["value"],
+                            "unit": "GB/s", "frac": achieved / peak["value"],
+                            "traffic": traffic, "peak_source": peak["source"],
+                            "kernel": f"block_kernel<double,plain,T={block_T}>",
+                            "algorithmic_bytes_per_launch": alg_bytes,
+                            "avg_launch_s": avg, "kernel_share_of_step": share,
+                            "note": "algorithmic bytes count 24 B per point-update per inner "
+                                    "step; temporal blocking fuses T steps per HBM pass, so "
+                                    "frac can exceed 1 (SURVEY.md §8(d))"},
+               "cpu_baseline": cpu, "time_to_tol": ttt}
+    return out
+
+
+def _peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return {"value": float(json.loads(p.read_text())["hbm_gbs"]), "source": "measured"}
+    except Exception:  # noqa: BLE001
+        return {"value": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def _ncu_traffic(block_T):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_block_kernel.json), or None."""
+    p = ROOT / "profiles" / "ncu_block_kernel.json"
+    try:
+        d = json.loads(p.read_text())
+        if int(d.get("block_T", -1)) == block_T:
+            return float(d["dram_bytes_per_launch"])
+    except Exception:  # noqa: BLE001
+        pass
+    return None
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--block-T", dest="block_T", type=int, default=0)
+    ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=5)
+    ap.add_argument("--no-time-to-tol", dest="time_to_tol", action="store_false")
+    ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    rank, world, local = dist_setup()
+    if args.impl == "reference":
+        out = run_reference(args, rank, world)
+    else:
+        out = run_gpu(args, rank, world, local)
+    if rank == 0 and out is not None:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,174 @@
+/*
+ * richgpu.h — C-ABI of the B200 (sm_100a) Richardson(m) solve-loop library.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `richlab` (arXiv 2412.08076).  The reference is pure Python; its hot path
+ * calls SciPy's CSR matvec, NumPy ufuncs, BLAS ddot and pocketfft.  Each
+ * entry point below replaces one of those reference call sites (cited as
+ * file:line into /root/reference/pkg/src/richlab/).  The Python shim in
+ * paper_2412_08076_b200/ binds these with ctypes.
+ *
+ * Conventions
+ *  - Plain C types only.  Every array pointer is CALLER-OWNED DEVICE memory
+ *    unless the comment says "host".  `stream` is a cudaStream_t passed as
+ *    void* (NULL = legacy default stream).
+ *  - Grids: one "system" is the (side x side) interior of an (side+1)-cell
+ *    Dirichlet grid, flattened row-major with x the slow axis:
+ *    index = (ix-1)*side + (iy-1)   (problems.py:131-133).  A batch of B
+ *    systems is B such vectors back to back.
+ *  - Scalar type of vectors follows the operator dtype: RG_F32 -> float,
+ *    RG_F64 -> double, RG_C128 -> interleaved (re, im) doubles.
+ *  - Return value: RG_OK (0) or a negative rg_err; rg_last_error() gives the
+ *    text (thread-local).  Numerical divergence is NOT a call failure: it is
+ *    reported per system through rg_report.status (reference
+ *    DivergenceError, richardson.py:20-23,126-129).
+ *  - Handles are immutable after creation except rg_solver (one solve in
+ *    flight per solver).  Operators may be shared by concurrent solvers
+ *    (mirrors "multiple solves over shared immutable A may run concurrently").
+ */
+#ifndef RICHGPU_H
+#define RICHGPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RG_ABI_VERSION 1
+
+enum rg_dtype   { RG_F32 = 1, RG_F64 = 2, RG_C128 = 3 };
+/* Operator kinds.  CONST9: one 9-point stencil per system (bilinear-FEM
+ * anisotropic operator, problems.py:121-154).  DIAG5: 5-point stencil with
+ * constant off-diagonals and a per-node diagonal (damped Helmholtz,
+ * problems.py:174-200).  VAR9: 9 per-node coefficient planes (Galerkin
+ * coarse operators, multigrid.py:62-68). */
+enum rg_kind    { RG_CONST9 = 1, RG_DIAG5 = 2, RG_VAR9 = 3 };
+/* schedules.py:8 VARIANTS */
+enum rg_variant { RG_PLAIN = 0, RG_MOM = 1, RG_NAG = 2, RG_NAGEX = 3 };
+/* precond.py:71-77 weighted Jacobi (scale = relax/diag).  SCALAR: one scale
+ * per system (constant diagonal); FIELD: one scale per node. */
+enum rg_precond { RG_PRECOND_NONE = 0, RG_PRECOND_JACOBI_SCALAR = 1,
+                  RG_PRECOND_JACOBI_FIELD = 2 };
+/* richardson.py:77-90 `check` */
+enum rg_check   { RG_CHECK_OUTER = 0, RG_CHECK_INNER = 1 };
+enum rg_status  { RG_ACTIVE = 0, RG_CONVERGED = 1, RG_DIVERGED = 2,
+                  RG_MAXED = 3 };
+enum rg_err     { RG_OK = 0, RG_EINVAL = -1, RG_ESIZE = -2, RG_ENULL = -3,
+                  RG_EUNSUPPORTED = -4, RG_ECUDA = -5, RG_ESTATE = -6 };
+
+typedef struct rg_op rg_op;
+typedef struct rg_solver rg_solver;
+
+/* Operator description.  Coefficient arrays are device pointers that must
+ * outlive the handle (no copy is taken).
+ *   CONST9 : stencil = [batch][9] in CSR column order (di,dj) =
+ *            (-1,-1),(-1,0),(-1,1),(0,-1),(0,0),(0,1),(1,-1),(1,0),(1,1)
+ *   DIAG5  : stencil = [batch][4] off-diagonals in CSR order
+ *            (-1,0),(0,-1),(0,1),(1,0);  diag = [batch][side*side]
+ *   VAR9   : stencil = [batch][9][side*side] planes, same offset order,
+ *            absent CSR entries stored as 0.                               */
+typedef struct rg_op_desc {
+    int dtype;
+    int kind;
+    int batch;
+    int side;
+    const void* stencil;
+    const void* diag;
+} rg_op_desc;
+
+/* Weight schedule for all systems of a batch (schedules.py:11-54).
+ * omega/alpha/alpha_tilde are device double arrays [batch][m]; alpha and
+ * alpha_tilde may be NULL for RG_PLAIN.  scale: device array of the op's
+ * scalar type, [batch] (SCALAR) or [batch][side*side] (FIELD).            */
+typedef struct rg_sched {
+    int variant;
+    int m;
+    const double* omega;
+    const double* alpha;
+    const double* alpha_tilde;
+    int precond;
+    const void* scale;
+} rg_sched;
+
+/* Per-system outcome of a solve (richardson.py:38-46 SolveReport plus the
+ * DivergenceError payload).  Filled on the host by rg_solver_report. */
+typedef struct rg_report {
+    int status;            /* rg_status */
+    int iterations;        /* outer sweeps, a trailing partial sweep counts */
+    int inner_iterations;  /* also the DivergenceError.inner_iteration */
+    int ans_buf;           /* which of the two u buffers holds the answer */
+    double final_relative_residual;
+    double trace0;
+    double fnorm;
+    double bad_rel;        /* relative residual that triggered divergence */
+} rg_report;
+
+int         rg_version(void);
+const char* rg_last_error(void);
+
+/* ---- operator (sparse.py:13-133 SparseMatrix, duck-typed by the solvers) */
+int rg_op_create(rg_op** out, const rg_op_desc* desc);
+int rg_op_destroy(rg_op* op);
+
+/* y = A x for every system (sparse.py:101-106 -> scipy csr_matvec).  Summed
+ * in CSR column order without FMA contraction: bitwise equal to SciPy. */
+int rg_matvec(const rg_op* A, const void* x, void* y, void* stream);
+
+/* r = f - A u (r may be NULL) and norm2[b] = ||r_b||^2 (device, may be NULL)
+ * (richardson.py:105-106,124-125; np.linalg.norm -> deterministic
+ * fixed-order reduction, not bitwise BLAS). */
+int rg_residual(const rg_op* A, const void* u, const void* f, void* r,
+                double* norm2, void* stream);
+
+/* One inner update of _inner_update (richardson.py:49-59) for every system:
+ *   plain/mom: r = f - A u ;  nag/nagex: r = f - A (u + at_i v)
+ *   v_out = a_i v + w_i B^{-1} r ;  u_out = u + v_out
+ * u_in/u_out and v_in/v_out must not alias (neighbour reads).  v_in may be
+ * NULL (treated as 0) for plain.  If nonfinite_at (device int[batch]) is
+ * given, the first `tag` at which u_out or v_out held a non-finite entry is
+ * recorded with atomicMin (outer_sweep's check, richardson.py:67-70). */
+int rg_inner_update(const rg_op* A, const rg_sched* s, int i,
+                    const void* u_in, const void* v_in,
+                    void* u_out, void* v_out, const void* f,
+                    int* nonfinite_at, int tag, void* stream);
+
+/* ---- solve_stationary engine (richardson.py:77-141) ----------------------
+ * A solver owns device workspace (per-system status, trace, reduction
+ * partials) and runs the whole loop on the device: convergence, divergence
+ * and max_outer decisions are taken by the last CTA of each launch, and
+ * finished systems are skipped by later launches, so the host only polls.
+ * Iterates live in two caller-owned ping-pong buffers u0/u1 (and v0/v1 for
+ * mom/nag/nagex); rg_report.ans_buf says which one holds the answer.
+ * block_T: temporal-blocking depth (inner steps fused per HBM pass) for the
+ * CONST9 real path; 0 = automatic, 1 = off.                              */
+int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s,
+                     double tol, int max_outer, int check, int block_T);
+int rg_solver_destroy(rg_solver* S);
+/* u0 holds the initial guess on entry; u1, v0, v1 are scratch. v0/v1 may be
+ * NULL for plain. Computes ||f||, the initial residual and trace[0]. */
+int rg_solver_begin(rg_solver* S, void* u0, void* u1, void* v0, void* v1,
+                    const void* f, void* stream);
+/* Enqueue exactly one kernel launch of the sweep schedule (no host sync).
+ * *steps_out = inner steps it covers (0 once max_outer sweeps are queued). */
+int rg_solver_step(rg_solver* S, void* stream, int* steps_out);
+/* Enqueue n_sweeps outer sweeps (or up to max_outer) plus the trailing
+ * residual check; no host sync. */
+int rg_solver_run(rg_solver* S, int n_sweeps, void* stream);
+/* Enqueue the residual check of the current iterate (resolves the lagged
+ * convergence test of the last queued sweep). */
+int rg_solver_flush(rg_solver* S, void* stream);
+/* Synchronise `stream`, copy the per-system state to the host.
+ * *n_active = systems still iterating; *done = 1 when nothing is left to do
+ * (all systems finished or max_outer sweeps queued and flushed). */
+int rg_solver_poll(rg_solver* S, void* stream, int* n_active, int* done);
+int rg_solver_report(const rg_solver* S, int b, rg_report* out);
+/* Copy trace[0..iterations] of system b into host buffer out (cap entries). */
+int rg_solver_trace(const rg_solver* S, int b, double* out, int cap,
+                    int* n_out);
+/* Inner steps queued so far and the temporal-blocking depth in use. */
+int rg_solver_info(const rg_solver* S, long long* steps_queued,
+                   int* block_T, int* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RICHGPU_H */

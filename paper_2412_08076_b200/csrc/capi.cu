@@ -1,0 +1,587 @@
+// capi.cu — extern "C" boundary of librichgpu (declared in include/richgpu.h).
+//
+// Host-side dispatch, argument validation and the solve_stationary launch
+// planner.  No torch types cross this boundary: plain pointers, ints and a
+// cudaStream_t passed as void*.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <string>
+#include <vector>
+
+#include "../../include/richgpu.h"
+#include "block.cuh"
+
+using namespace rg;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+    char b[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(b, sizeof b, fmt, ap);
+    va_end(ap);
+    g_err = b;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                              \
+    do {                                                                            \
+        cudaError_t e_ = (expr);                                                    \
+        if (e_ != cudaSuccess)                                                      \
+            return fail(RG_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),  \
+                        __FILE__, __LINE__);                                        \
+    } while (0)
+
+#define LAUNCH_CHECK()                                                              \
+    do {                                                                            \
+        cudaError_t e_ = cudaGetLastError();                                        \
+        if (e_ != cudaSuccess)                                                      \
+            return fail(RG_ECUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                        \
+    } while (0)
+
+struct rg_op {
+    rg_op_desc d;
+    int P;
+};
+
+struct rg_solver {
+    const rg_op* A;
+    rg_sched s;
+    SolveCfg cfg;
+    int check;
+    int block_T;
+    bool use_block;
+    SysState* d_st;
+    double* d_trace;
+    double* d_part;
+    int ncta_cap;
+    int trace_stride;
+    SysState* h_st;
+    void* u[2];
+    void* v[2];
+    const void* f;
+    long long k;
+    long long kmax;
+    long long flushed_k;
+    int cur;
+    int launches;
+    bool need_flush;
+    bool begun;
+};
+
+// ---------------------------------------------------------------- helpers
+static size_t scalar_bytes(int dtype) {
+    return dtype == RG_F32 ? 4 : dtype == RG_F64 ? 8 : 16;
+}
+
+static dim3 step_grid(const rg_op* A) {
+    const int side = A->d.side;
+    return dim3((side + STEP_BX - 1) / STEP_BX, (side + STEP_BY - 1) / STEP_BY, A->d.batch);
+}
+
+template <typename S>
+static OpView<S> view(const rg_op* A) {
+    OpView<S> v;
+    v.stencil = (const S*)A->d.stencil;
+    v.diag = (const S*)A->d.diag;
+    v.side = A->d.side;
+    v.P = A->P;
+    return v;
+}
+
+// ------------------------------------------------------- step1 dispatch
+template <typename S, int KIND>
+static int launch_step1_k(const rg_op* A, StepArgs<S>& a, cudaStream_t st) {
+    step1_kernel<S, KIND><<<step_grid(A), dim3(STEP_BX, STEP_BY), 0, st>>>(a);
+    LAUNCH_CHECK();
+    return RG_OK;
+}
+
+template <typename S>
+static int launch_step1(const rg_op* A, StepArgs<S>& a, cudaStream_t st) {
+    switch (A->d.kind) {
+        case RG_CONST9: return launch_step1_k<S, K_CONST9>(A, a, st);
+        case RG_DIAG5: return launch_step1_k<S, K_DIAG5>(A, a, st);
+        case RG_VAR9: return launch_step1_k<S, K_VAR9>(A, a, st);
+    }
+    return fail(RG_EINVAL, "bad operator kind %d", A->d.kind);
+}
+
+// Generic "one step" request independent of the scalar type.
+struct StepReq {
+    const void *u_in, *v_in, *f, *scale;
+    void *u_out, *v_out, *r_out;
+    const double *omega, *alpha, *atil;
+    int m, i, variant, precond, update, norm_u, use_status;
+    int* nonfinite_at;
+    int tag;
+    double* partials;
+    EpiArgs epi;
+};
+
+template <typename S>
+static int do_step1(const rg_op* A, const StepReq& q, cudaStream_t st) {
+    StepArgs<S> a;
+    a.A = view<S>(A);
+    a.u_in = (const S*)q.u_in;
+    a.v_in = (const S*)q.v_in;
+    a.u_out = (S*)q.u_out;
+    a.v_out = (S*)q.v_out;
+    a.f = (const S*)q.f;
+    a.r_out = (S*)q.r_out;
+    a.omega = q.omega;
+    a.alpha = q.alpha;
+    a.atil = q.atil;
+    a.scale = (const S*)q.scale;
+    a.m = q.m;
+    a.i = q.i;
+    a.variant = q.variant;
+    a.precond = q.precond;
+    a.update = q.update;
+    a.norm_u = q.norm_u;
+    a.use_status = q.use_status;
+    a.nonfinite_at = q.nonfinite_at;
+    a.tag = q.tag;
+    a.partials = q.partials;
+    a.epi = q.epi;
+    return launch_step1<S>(A, a, st);
+}
+
+static int step1(const rg_op* A, const StepReq& q, cudaStream_t st) {
+    switch (A->d.dtype) {
+        case RG_F32: return do_step1<float>(A, q, st);
+        case RG_F64: return do_step1<double>(A, q, st);
+        case RG_C128: return do_step1<double2>(A, q, st);
+    }
+    return fail(RG_EINVAL, "bad dtype %d", A->d.dtype);
+}
+
+// ------------------------------------------------------- block dispatch
+template <typename S>
+static int do_block(rg_solver* S_, int T, int norm_first_u, cudaStream_t st) {
+    const rg_op* A = S_->A;
+    BlockArgs<S> a;
+    a.stencil = (const S*)A->d.stencil;
+    a.side = A->d.side;
+    a.P = A->P;
+    a.u_in = (const S*)S_->u[S_->cur];
+    a.u_out = (S*)S_->u[S_->cur ^ 1];
+    a.v_in = (const S*)S_->v[S_->cur];
+    a.v_out = (S*)S_->v[S_->cur ^ 1];
+    a.f = (const S*)S_->f;
+    a.omega = S_->s.omega;
+    a.alpha = S_->s.alpha;
+    a.atil = S_->s.alpha_tilde;
+    a.scale = S_->s.precond == RG_PRECOND_JACOBI_SCALAR ? (const S*)S_->s.scale : nullptr;
+    a.m = S_->s.m;
+    a.k0 = (int)S_->k;
+    const bool nag = S_->s.variant >= RG_NAG;
+    a.norm_first_u = norm_first_u;
+    a.norm_every = nag ? 0 : 1;
+    EpiArgs& e = a.epi;
+    e.st = S_->d_st;
+    e.trace = S_->d_trace;
+    e.trace_stride = S_->trace_stride;
+    e.partials = S_->d_part;
+    e.ncta_cap = S_->ncta_cap;
+    e.cfg = S_->cfg;
+    e.j0 = (int)S_->k;
+    e.nslots = nag ? (norm_first_u ? 1 : 0) : T;
+    e.with_f = 0;
+    e.buf = S_->cur;
+    cudaError_t err;
+    switch (S_->s.variant) {
+        case RG_PLAIN: err = launch_block<S, V_PLAIN>(a, T, A->d.batch, st); break;
+        case RG_MOM: err = launch_block<S, V_MOM>(a, T, A->d.batch, st); break;
+        default: err = launch_block<S, V_NAG>(a, T, A->d.batch, st); break;
+    }
+    if (err != cudaSuccess) return fail(RG_ECUDA, "block sweep launch: %s", cudaGetErrorString(err));
+    return RG_OK;
+}
+
+// ------------------------------------------------------------- validation
+static int check_op(const rg_op* A) {
+    if (!A) return fail(RG_ENULL, "null operator");
+    return RG_OK;
+}
+
+static int check_sched(const rg_op* A, const rg_sched* s) {
+    if (!s) return fail(RG_ENULL, "null schedule");
+    if (s->m < 1) return fail(RG_EINVAL, "schedule needs at least one weight (m=%d)", s->m);
+    if (s->variant < RG_PLAIN || s->variant > RG_NAGEX)
+        return fail(RG_EINVAL, "unknown variant %d", s->variant);
+    if (!s->omega) return fail(RG_ENULL, "null omega");
+    if (s->variant != RG_PLAIN && !s->alpha) return fail(RG_ENULL, "variant needs alpha");
+    if (s->variant >= RG_NAG && !s->alpha_tilde) return fail(RG_ENULL, "variant needs alpha_tilde");
+    if (s->precond < RG_PRECOND_NONE || s->precond > RG_PRECOND_JACOBI_FIELD)
+        return fail(RG_EINVAL, "unknown preconditioner %d", s->precond);
+    if (s->precond != RG_PRECOND_NONE && !s->scale) return fail(RG_ENULL, "Jacobi needs scale");
+    (void)A;
+    return RG_OK;
+}
+
+// ==================================================================== C ABI
+extern "C" {
+
+int rg_version(void) { return RG_ABI_VERSION; }
+
+const char* rg_last_error(void) { return g_err.c_str(); }
+
+int rg_op_create(rg_op** out, const rg_op_desc* d) {
+    if (!out || !d) return fail(RG_ENULL, "null argument");
+    if (d->dtype != RG_F32 && d->dtype != RG_F64 && d->dtype != RG_C128)
+        return fail(RG_EINVAL, "bad dtype %d", d->dtype);
+    if (d->kind != RG_CONST9 && d->kind != RG_DIAG5 && d->kind != RG_VAR9)
+        return fail(RG_EINVAL, "bad operator kind %d", d->kind);
+    if (d->batch < 1 || d->side < 1) return fail(RG_ESIZE, "batch=%d side=%d", d->batch, d->side);
+    if ((long long)d->side * d->side > (1ll << 30)) return fail(RG_ESIZE, "grid too large");
+    if (!d->stencil) return fail(RG_ENULL, "null stencil");
+    if (d->kind == RG_DIAG5 && !d->diag) return fail(RG_ENULL, "DIAG5 needs a diagonal");
+    rg_op* A = new rg_op;
+    A->d = *d;
+    A->P = d->side * d->side;
+    *out = A;
+    return RG_OK;
+}
+
+int rg_op_destroy(rg_op* A) {
+    delete A;
+    return RG_OK;
+}
+
+int rg_matvec(const rg_op* A, const void* x, void* y, void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if (!x || !y) return fail(RG_ENULL, "null vector");
+    cudaStream_t st = (cudaStream_t)stream;
+    const dim3 g = step_grid(A), blk(STEP_BX, STEP_BY);
+#define MV(S, K) matvec_kernel<S, K><<<g, blk, 0, st>>>(view<S>(A), (const S*)x, (S*)y)
+    switch (A->d.dtype * 10 + A->d.kind) {
+        case RG_F32 * 10 + RG_CONST9: MV(float, K_CONST9); break;
+        case RG_F32 * 10 + RG_DIAG5: MV(float, K_DIAG5); break;
+        case RG_F32 * 10 + RG_VAR9: MV(float, K_VAR9); break;
+        case RG_F64 * 10 + RG_CONST9: MV(double, K_CONST9); break;
+        case RG_F64 * 10 + RG_DIAG5: MV(double, K_DIAG5); break;
+        case RG_F64 * 10 + RG_VAR9: MV(double, K_VAR9); break;
+        case RG_C128 * 10 + RG_CONST9: MV(double2, K_CONST9); break;
+        case RG_C128 * 10 + RG_DIAG5: MV(double2, K_DIAG5); break;
+        case RG_C128 * 10 + RG_VAR9: MV(double2, K_VAR9); break;
+        default: return fail(RG_EINVAL, "bad dtype/kind");
+    }
+#undef MV
+    LAUNCH_CHECK();
+    return RG_OK;
+}
+
+int rg_residual(const rg_op* A, const void* u, const void* f, void* r, double* norm2,
+                void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if (!u || !f) return fail(RG_ENULL, "null vector");
+    cudaStream_t st = (cudaStream_t)stream;
+    StepReq q;
+    memset(&q, 0, sizeof q);
+    q.u_in = u;
+    q.f = f;
+    q.r_out = r;
+    q.m = 1;
+    q.norm_u = norm2 ? 1 : 0;
+    const dim3 g = step_grid(A);
+    const int ncta = g.x * g.y;
+    if (norm2) {
+        CUDA_TRY(cudaMallocAsync((void**)&q.partials, sizeof(double) * ncta * A->d.batch, st));
+    }
+    rc = step1(A, q, st);
+    if (rc == RG_OK && norm2) {
+        sum_partials_kernel<256><<<A->d.batch, 256, 0, st>>>(q.partials, ncta, norm2);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(RG_ECUDA, "reduce launch: %s", cudaGetErrorString(e));
+    }
+    if (norm2) CUDA_TRY(cudaFreeAsync(q.partials, st));
+    return rc;
+}
+
+int rg_inner_update(const rg_op* A, const rg_sched* s, int i, const void* u_in, const void* v_in,
+                    void* u_out, void* v_out, const void* f, int* nonfinite_at, int tag,
+                    void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if ((rc = check_sched(A, s))) return rc;
+    if (i < 0 || i >= s->m) return fail(RG_EINVAL, "inner index %d outside [0, %d)", i, s->m);
+    if (!u_in || !u_out || !f) return fail(RG_ENULL, "null vector");
+    if (u_in == u_out) return fail(RG_EINVAL, "u_in and u_out must not alias");
+    if (s->variant >= RG_NAG && v_in && v_in == v_out)
+        return fail(RG_EINVAL, "v_in and v_out must not alias for nag/nagex");
+    StepReq q;
+    memset(&q, 0, sizeof q);
+    q.u_in = u_in;
+    q.v_in = v_in;
+    q.u_out = u_out;
+    q.v_out = v_out;
+    q.f = f;
+    q.omega = s->omega;
+    q.alpha = s->alpha;
+    q.atil = s->alpha_tilde;
+    q.scale = s->scale;
+    q.m = s->m;
+    q.i = i;
+    q.variant = s->variant;
+    q.precond = s->precond;
+    q.update = 1;
+    q.nonfinite_at = nonfinite_at;
+    q.tag = tag;
+    return step1(A, q, (cudaStream_t)stream);
+}
+
+int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double tol,
+                     int max_outer, int check, int block_T) {
+    if (!out) return fail(RG_ENULL, "null out");
+    int rc = check_op(A);
+    if (rc) return rc;
+    if ((rc = check_sched(A, s))) return rc;
+    if (!(tol > 0)) return fail(RG_EINVAL, "tol must be positive");
+    if (check != RG_CHECK_OUTER && check != RG_CHECK_INNER)
+        return fail(RG_EINVAL, "check must be 'outer' or 'inner'");
+    if (max_outer < 0) return fail(RG_EINVAL, "max_outer must be >= 0");
+    if ((long long)max_outer * s->m > 2000000000ll) return fail(RG_ESIZE, "max_outer*m too large");
+    if (block_T < 0 || block_T > 8) return fail(RG_EINVAL, "block_T must be in [0, 8]");
+    rg_solver* S = new rg_solver;
+    memset(S, 0, sizeof *S);
+    S->A = A;
+    S->s = *s;
+    S->cfg.tol = tol;
+    S->cfg.div_factor = 1e12;
+    S->cfg.m = s->m;
+    S->cfg.max_outer = max_outer;
+    S->cfg.check_inner = check == RG_CHECK_INNER;
+    S->check = check;
+    const bool real = A->d.dtype == RG_F32 || A->d.dtype == RG_F64;
+    S->use_block = real && A->d.kind == RG_CONST9 && check == RG_CHECK_OUTER &&
+                   s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
+    S->block_T = block_T == 0 ? 4 : block_T;
+    if (!S->use_block) S->block_T = 1;
+    S->kmax = (long long)max_outer * s->m;
+    const dim3 g = step_grid(A);
+    int cap = g.x * g.y;
+    for (int T = 1; T <= 8; ++T) {
+        const int nt = block_ntiles(A->d.side, T, nullptr);
+        if (nt > cap) cap = nt;
+    }
+    S->ncta_cap = cap;
+    S->trace_stride = max_outer + 1;
+    const int B = A->d.batch;
+    cudaError_t e;
+    if ((e = cudaMalloc((void**)&S->d_st, sizeof(SysState) * B)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&S->d_trace, sizeof(double) * B * (size_t)S->trace_stride)) !=
+            cudaSuccess ||
+        (e = cudaMalloc((void**)&S->d_part, sizeof(double) * B * (size_t)NSLOT * cap)) !=
+            cudaSuccess ||
+        (e = cudaMallocHost((void**)&S->h_st, sizeof(SysState) * B)) != cudaSuccess) {
+        cudaFree(S->d_st);
+        cudaFree(S->d_trace);
+        cudaFree(S->d_part);
+        delete S;
+        return fail(RG_ECUDA, "solver workspace: %s", cudaGetErrorString(e));
+    }
+    *out = S;
+    return RG_OK;
+}
+
+int rg_solver_destroy(rg_solver* S) {
+    if (!S) return RG_OK;
+    cudaFree(S->d_st);
+    cudaFree(S->d_trace);
+    cudaFree(S->d_part);
+    cudaFreeHost(S->h_st);
+    delete S;
+    return RG_OK;
+}
+
+static EpiArgs solver_epi(rg_solver* S, int j0, int nslots, int with_f) {
+    EpiArgs e;
+    e.st = S->d_st;
+    e.trace = S->d_trace;
+    e.trace_stride = S->trace_stride;
+    e.partials = S->d_part;
+    e.ncta_cap = S->ncta_cap;
+    e.cfg = S->cfg;
+    e.j0 = j0;
+    e.nslots = nslots;
+    e.with_f = with_f;
+    e.buf = S->cur;
+    return e;
+}
+
+int rg_solver_begin(rg_solver* S, void* u0, void* u1, void* v0, void* v1, const void* f,
+                    void* stream) {
+    if (!S) return fail(RG_ENULL, "null solver");
+    if (!u0 || !u1 || !f) return fail(RG_ENULL, "null vector");
+    if (S->s.variant != RG_PLAIN && (!v0 || !v1)) return fail(RG_ENULL, "variant needs v0/v1");
+    cudaStream_t st = (cudaStream_t)stream;
+    const rg_op* A = S->A;
+    const size_t vbytes = scalar_bytes(A->d.dtype) * (size_t)A->P * A->d.batch;
+    S->u[0] = u0;
+    S->u[1] = u1;
+    S->v[0] = v0;
+    S->v[1] = v1;
+    S->f = f;
+    S->k = 0;
+    S->cur = 0;
+    S->launches = 0;
+    S->flushed_k = 0;
+    S->need_flush = false;
+    CUDA_TRY(cudaMemsetAsync(S->d_st, 0, sizeof(SysState) * A->d.batch, st));
+    CUDA_TRY(cudaMemsetAsync(S->d_trace, 0, sizeof(double) * A->d.batch * (size_t)S->trace_stride, st));
+    if (v0) CUDA_TRY(cudaMemsetAsync(v0, 0, vbytes, st));  // v = 0 at entry (:95)
+    StepReq q;
+    memset(&q, 0, sizeof q);
+    q.u_in = u0;
+    q.f = f;
+    q.m = S->s.m;
+    q.norm_u = 1;
+    q.use_status = 0;
+    q.epi = solver_epi(S, 0, 1, 1);
+    int rc = step1(A, q, st);
+    if (rc) return rc;
+    S->begun = true;
+    return RG_OK;
+}
+
+int rg_solver_step(rg_solver* S, void* stream, int* steps_out) {
+    if (!S) return fail(RG_ENULL, "null solver");
+    if (!S->begun) return fail(RG_ESTATE, "rg_solver_begin not called");
+    if (steps_out) *steps_out = 0;
+    if (S->k >= S->kmax) return RG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int m = S->s.m;
+    const int i = (int)(S->k % m);
+    const bool nag = S->s.variant >= RG_NAG;
+    const bool boundary_norm = nag && i == 0 && S->k > 0 && S->flushed_k != S->k;
+    int T = 1;
+    int rc;
+    if (S->use_block) {
+        T = S->block_T < (m - i) ? S->block_T : (m - i);
+        if (S->A->d.dtype == RG_F64) rc = do_block<double>(S, T, boundary_norm ? 1 : 0, st);
+        else rc = do_block<float>(S, T, boundary_norm ? 1 : 0, st);
+    } else {
+        StepReq q;
+        memset(&q, 0, sizeof q);
+        q.u_in = S->u[S->cur];
+        q.u_out = S->u[S->cur ^ 1];
+        q.v_in = S->v[S->cur];
+        q.v_out = S->v[S->cur ^ 1];
+        q.f = S->f;
+        q.omega = S->s.omega;
+        q.alpha = S->s.alpha;
+        q.atil = S->s.alpha_tilde;
+        q.scale = S->s.scale;
+        q.m = m;
+        q.i = i;
+        q.variant = S->s.variant;
+        q.precond = S->s.precond;
+        q.update = 1;
+        q.norm_u = (!nag || S->cfg.check_inner || boundary_norm) ? 1 : 0;
+        q.use_status = 1;
+        q.epi = solver_epi(S, (int)S->k, q.norm_u, 0);
+        rc = step1(S->A, q, st);
+    }
+    if (rc) return rc;
+    S->cur ^= 1;
+    S->k += T;
+    S->launches += 1;
+    S->need_flush = true;
+    if (steps_out) *steps_out = T;
+    return RG_OK;
+}
+
+int rg_solver_flush(rg_solver* S, void* stream) {
+    if (!S) return fail(RG_ENULL, "null solver");
+    if (!S->begun) return fail(RG_ESTATE, "rg_solver_begin not called");
+    if (!S->need_flush) return RG_OK;
+    S->need_flush = false;
+    const int m = S->s.m;
+    const bool nag = S->s.variant >= RG_NAG;
+    if (nag && !S->cfg.check_inner && (S->k % m) != 0) return RG_OK;  // no test mid-sweep
+    StepReq q;
+    memset(&q, 0, sizeof q);
+    q.u_in = S->u[S->cur];
+    q.f = S->f;
+    q.m = m;
+    q.norm_u = 1;
+    q.use_status = 1;
+    q.epi = solver_epi(S, (int)S->k, 1, 0);
+    int rc = step1(S->A, q, (cudaStream_t)stream);
+    if (rc) return rc;
+    S->flushed_k = S->k;
+    return RG_OK;
+}
+
+int rg_solver_run(rg_solver* S, int n_sweeps, void* stream) {
+    if (!S) return fail(RG_ENULL, "null solver");
+    if (!S->begun) return fail(RG_ESTATE, "rg_solver_begin not called");
+    if (n_sweeps < 1) return fail(RG_EINVAL, "n_sweeps must be >= 1");
+    const long long m = S->s.m;
+    long long target = (S->k / m + n_sweeps) * m;
+    if (target > S->kmax) target = S->kmax;
+    while (S->k < target) {
+        int steps = 0;
+        int rc = rg_solver_step(S, stream, &steps);
+        if (rc) return rc;
+        if (steps == 0) break;
+    }
+    return rg_solver_flush(S, stream);
+}
+
+int rg_solver_poll(rg_solver* S, void* stream, int* n_active, int* done) {
+    if (!S) return fail(RG_ENULL, "null solver");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int B = S->A->d.batch;
+    CUDA_TRY(cudaMemcpyAsync(S->h_st, S->d_st, sizeof(SysState) * B, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int act = 0;
+    for (int b = 0; b < B; ++b) act += S->h_st[b].status == ST_ACTIVE;
+    if (n_active) *n_active = act;
+    if (done) *done = (act == 0) || (S->k >= S->kmax && !S->need_flush);
+    return RG_OK;
+}
+
+int rg_solver_report(const rg_solver* S, int b, rg_report* out) {
+    if (!S || !out) return fail(RG_ENULL, "null argument");
+    if (b < 0 || b >= S->A->d.batch) return fail(RG_ESIZE, "system %d out of range", b);
+    const SysState& s = S->h_st[b];
+    out->status = s.status;
+    out->iterations = s.outer;
+    out->inner_iterations = s.inner;
+    out->ans_buf = s.ans_buf;
+    out->final_relative_residual = s.rel;
+    out->trace0 = s.trace0;
+    out->fnorm = s.fnorm;
+    out->bad_rel = s.bad_rel;
+    return RG_OK;
+}
+
+int rg_solver_trace(const rg_solver* S, int b, double* out, int cap, int* n_out) {
+    if (!S || !out) return fail(RG_ENULL, "null argument");
+    if (b < 0 || b >= S->A->d.batch) return fail(RG_ESIZE, "system %d out of range", b);
+    int n = S->h_st[b].outer + 1;
+    if (n > S->trace_stride) n = S->trace_stride;
+    if (n > cap) n = cap;
+    CUDA_TRY(cudaMemcpy(out, S->d_trace + (size_t)b * S->trace_stride, sizeof(double) * n,
+                        cudaMemcpyDeviceToHost));
+    if (n_out) *n_out = n;
+    return RG_OK;
+}
+
+int rg_solver_info(const rg_solver* S, long long* steps_queued, int* block_T, int* launches) {
+    if (!S) return fail(RG_ENULL, "null solver");
+    if (steps_queued) *steps_queued = S->k;
+    if (block_T) *block_T = S->block_T;
+    if (launches) *launches = S->launches;
+    return RG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,309 @@
+"""Drop-in GPU versions of the reference solve loop (richardson.py).
+
+    solve_stationary(A, f, schedule, P=None, tol=1e-6, max_outer=100_000,
+                     u0=None, check="outer")                -> (u, SolveReport)
+    solve_stationary_batched(A, F, schedules, P=None, ...)  -> [(u, report), ...]
+    outer_sweep(A, f, state, schedule, P=None)              -> state
+    inner_update(A, f, u, v, i, schedule, P=None)           -> (u, v)
+
+Same signatures, return types, SolveReport fields, error types and messages
+as richardson.py:49-141.  `A` is a GpuStencilOperator or any assembled CSR
+of a structured-grid operator (converted once); `f`, `u0`, `state.u/v` may be
+NumPy arrays (results come back as NumPy) or CUDA tensors (results stay on
+the device).  The whole iteration -- residual, Jacobi scaling, momentum
+update, fused norm reduction, convergence / divergence / max_outer decisions
+-- runs on the GPU; the host only polls a status word between batches of
+sweeps.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .errors import DimensionMismatch, DivergenceError, SolveReport, UnsupportedOperator
+from .operator import GpuStencilOperator, as_operator, precond_scale
+
+INT_MAX = 2**31 - 1
+
+
+# ---------------------------------------------------------------- helpers
+def _sched_list(schedules, B):
+    if isinstance(schedules, (list, tuple)):
+        if len(schedules) != B:
+            raise DimensionMismatch(f"{len(schedules)} schedules for {B} systems")
+        return list(schedules)
+    return [schedules] * B
+
+
+class DeviceSchedule:
+    """Device copy of B schedules sharing variant and m, plus the Jacobi
+    scale; keeps the tensors alive for the rg_sched struct."""
+
+    def __init__(self, op: GpuStencilOperator, schedules, P=None):
+        B = op.batch
+        sl = _sched_list(schedules, B)
+        variants = {s.variant for s in sl}
+        ms = {int(len(np.atleast_1d(s.omega))) for s in sl}
+        if len(variants) != 1 or len(ms) != 1:
+            raise ValueError("all systems of a batch must share variant and m")
+        self.variant = variants.pop()
+        if self.variant not in L.VARIANT_CODE:
+            raise ValueError(f"unknown variant {self.variant!r}")
+        self.m = ms.pop()
+        dev = op.device
+
+        def stack(attr):
+            return torch.as_tensor(np.stack([np.asarray(getattr(s, attr), dtype=np.float64)
+                                             for s in sl])).to(dev).contiguous()
+        self.omega = stack("omega")
+        self.alpha = stack("alpha")
+        self.alpha_tilde = stack("alpha_tilde")
+        self.precond = L.RG_PRECOND_NONE
+        self.scale = None
+        Ps = P if isinstance(P, (list, tuple)) else [P] * B
+        if len(Ps) != B:
+            raise DimensionMismatch(f"{len(Ps)} preconditioners for {B} systems")
+        if any(p is not None for p in Ps):
+            if any(p is None for p in Ps):
+                raise ValueError("mix of preconditioned and unpreconditioned systems in a batch")
+            scales = np.stack([np.asarray(precond_scale(p, op.P)).astype(op.np_dtype) for p in Ps])
+            if np.all(scales == scales[:, :1]):
+                self.precond = L.RG_PRECOND_JACOBI_SCALAR
+                self.scale = torch.as_tensor(np.ascontiguousarray(scales[:, 0])).to(dev)
+            else:
+                self.precond = L.RG_PRECOND_JACOBI_FIELD
+                self.scale = torch.as_tensor(np.ascontiguousarray(scales)).to(dev)
+        self.struct = L.rg_sched(L.VARIANT_CODE[self.variant], self.m,
+                                 self.omega.data_ptr(), self.alpha.data_ptr(),
+                                 self.alpha_tilde.data_ptr(), self.precond,
+                                 self.scale.data_ptr() if self.scale is not None else None)
+
+
+def _out(t, like_numpy):
+    return t.cpu().numpy() if like_numpy else t
+
+
+def _is_host(x):
+    return not (isinstance(x, torch.Tensor) and x.is_cuda)
+
+
+# ------------------------------------------------------------ the engine
+class StationarySolver:
+    """Device-resident solve_stationary for a batch of systems.
+
+    Holds the iterate ping-pong buffers, the schedule and the librichgpu
+    solver handle; `run()` drives the device loop to completion.  Exposed
+    for benchmarking (fixed numbers of sweeps, per-launch timing)."""
+
+    def __init__(self, op: GpuStencilOperator, schedules, P=None, tol=1e-6,
+                 max_outer=100_000, check="outer", block_T=0):
+        if tol <= 0:
+            raise ValueError("tol must be positive")
+        if check not in ("outer", "inner"):
+            raise ValueError("check must be 'outer' or 'inner'")
+        self.op = op
+        self.sched = DeviceSchedule(op, schedules, P)
+        self.tol, self.max_outer, self.check = tol, int(max_outer), check
+        self.lib = op._lib
+        h = C.c_void_p()
+        L.check(self.lib.rg_solver_create(
+            C.byref(h), op.handle, C.byref(self.sched.struct), float(tol), int(max_outer),
+            L.RG_CHECK_INNER if check == "inner" else L.RG_CHECK_OUTER, int(block_T)))
+        self._h = h
+        shp = (op.batch, op.P)
+        mk = lambda: torch.empty(shp, dtype=op.torch_dtype, device=op.device)  # noqa: E731
+        self.u = [mk(), mk()]
+        needv = self.sched.variant != "plain"
+        self.v = [mk(), mk()] if needv else [None, None]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self.lib.rg_solver_destroy(h)
+            self._h = None
+
+    def begin(self, f, u0=None):
+        self.f = self.op.to_device(f)
+        if u0 is None:
+            self.u[0].zero_()
+        else:
+            self.u[0].copy_(self.op.to_device(u0))
+        self.t0 = time.perf_counter()
+        L.check(self.lib.rg_solver_begin(self._h, L.ptr(self.u[0]), L.ptr(self.u[1]),
+                                         L.ptr(self.v[0]), L.ptr(self.v[1]), L.ptr(self.f),
+                                         L.stream_ptr()))
+
+    def step(self):
+        """Enqueue one kernel launch; returns the inner steps it covers."""
+        n = C.c_int()
+        L.check(self.lib.rg_solver_step(self._h, L.stream_ptr(), C.byref(n)))
+        return n.value
+
+    def flush(self):
+        L.check(self.lib.rg_solver_flush(self._h, L.stream_ptr()))
+
+    def run_sweeps(self, n):
+        L.check(self.lib.rg_solver_run(self._h, int(n), L.stream_ptr()))
+
+    def poll(self):
+        act, done = C.c_int(), C.c_int()
+        L.check(self.lib.rg_solver_poll(self._h, L.stream_ptr(), C.byref(act), C.byref(done)))
+        return act.value, bool(done.value)
+
+    def info(self):
+        k, T, nl = C.c_longlong(), C.c_int(), C.c_int()
+        L.check(self.lib.rg_solver_info(self._h, C.byref(k), C.byref(T), C.byref(nl)))
+        return k.value, T.value, nl.value
+
+    def run(self, first_batch=1, max_batch=64):
+        """Drive the device loop until every system finished."""
+        n = first_batch
+        while True:
+            self.run_sweeps(n)
+            active, done = self.poll()
+            if done:
+                return
+            n = min(2 * n, max_batch)
+
+    def report(self, b):
+        r = L.rg_report()
+        L.check(self.lib.rg_solver_report(self._h, int(b), C.byref(r)))
+        cap = max(1, r.iterations + 1)
+        buf = (C.c_double * cap)()
+        nout = C.c_int()
+        L.check(self.lib.rg_solver_trace(self._h, int(b), buf, cap, C.byref(nout)))
+        trace = np.frombuffer(buf, dtype=np.float64, count=nout.value).copy()
+        return r, trace
+
+    def result(self, b, like_numpy=True, wall=None):
+        """(u_b, SolveReport) or (None, DivergenceError) for system b."""
+        r, trace = self.report(b)
+        wall = time.perf_counter() - self.t0 if wall is None else wall
+        if r.status == L.RG_DIVERGED:
+            return None, DivergenceError(
+                f"residual blew up to {r.bad_rel:.3g} at inner iteration {r.inner_iterations}",
+                inner_iteration=r.inner_iterations)
+        if r.status == L.RG_ACTIVE:
+            raise RuntimeError("solve still running")
+        u = self.u[r.ans_buf][b]
+        rep = SolveReport(iterations=r.iterations, inner_iterations=r.inner_iterations,
+                          converged=r.status == L.RG_CONVERGED,
+                          final_relative_residual=float(r.final_relative_residual),
+                          wall_time=wall, trace=trace)
+        return _out(u.clone(), like_numpy), rep
+
+
+# --------------------------------------------------------------- public API
+def solve_stationary(A, f, schedule, P=None, tol=1e-6, max_outer=100_000, u0=None,
+                     check="outer", block_T=0):
+    """GPU drop-in for richardson.solve_stationary (richardson.py:77-141)."""
+    if tol <= 0:
+        raise ValueError("tol must be positive")
+    if check not in ("outer", "inner"):
+        raise ValueError("check must be 'outer' or 'inner'")
+    op = _op_for(A, f)
+    if op.batch != 1:
+        raise DimensionMismatch("use solve_stationary_batched for a batched operator")
+    _check_len(op, f)
+    S = StationarySolver(op, schedule, P, tol, max_outer, check, block_T)
+    S.begin(f, u0)
+    S.run()
+    u, rep = S.result(0, like_numpy=_is_host(f))
+    if isinstance(rep, DivergenceError):
+        raise rep
+    if isinstance(u, np.ndarray):
+        u = u.reshape(-1)
+    else:
+        u = u.reshape(-1)
+    return u, rep
+
+
+def solve_stationary_batched(A, F, schedules, P=None, tol=1e-6, max_outer=100_000, u0=None,
+                             check="outer", block_T=0, errors="return"):
+    """Solve B independent systems at once; per system equivalent to looping
+    the reference solve_stationary.  Returns a list of (u, SolveReport); a
+    system that diverged yields (None, DivergenceError) with errors="return"
+    or raises the first one (in system order) with errors="raise"."""
+    op = A if isinstance(A, GpuStencilOperator) else GpuStencilOperator.stack(
+        [as_operator(a) for a in A])
+    S = StationarySolver(op, schedules, P, tol, max_outer, check, block_T)
+    S.begin(F, u0)
+    S.run()
+    host = _is_host(F)
+    out = [S.result(b, like_numpy=host) for b in range(op.batch)]
+    if errors == "raise":
+        for u, rep in out:
+            if isinstance(rep, DivergenceError):
+                raise rep
+    return out
+
+
+def _op_for(A, f):
+    if isinstance(A, GpuStencilOperator):
+        return A
+    fd = f.dtype if isinstance(f, torch.Tensor) else np.asarray(f).dtype
+    if isinstance(fd, torch.dtype):
+        fd = {torch.float32: np.float32, torch.float64: np.float64,
+              torch.complex128: np.complex128}.get(fd, np.float64)
+    dt = np.promote_types(getattr(A, "dtype", np.float64), fd)  # richardson.py:93
+    if dt not in (np.float64, np.complex128):
+        dt = np.dtype(np.float64)
+    return GpuStencilOperator.from_sparse(A, dtype=dt)
+
+
+def _check_len(op, x):
+    n = x.numel() if isinstance(x, torch.Tensor) else np.asarray(x).size
+    if n != op.P * op.batch:
+        raise DimensionMismatch(
+            f"matrix has {op.ncols} columns but vector has length ({n},)")
+
+
+def inner_update(A, f, u, v, i, schedule, P=None):
+    """One inner update (richardson.py:49-59); returns (u, v) like the inputs."""
+    op = _op_for(A, f)
+    ds = DeviceSchedule(op, schedule, P)
+    host = _is_host(u)
+    ut, vt, ft = op.to_device(u), op.to_device(v), op.to_device(f)
+    un, vn = torch.empty_like(ut), torch.empty_like(vt)
+    L.check(op._lib.rg_inner_update(op.handle, C.byref(ds.struct), int(i), L.ptr(ut), L.ptr(vt),
+                                    L.ptr(un), L.ptr(vn), L.ptr(ft), None, 0, L.stream_ptr()))
+    shp = np.shape(u) if host else u.shape
+    return _out(un.reshape(shp), host), _out(vn.reshape(shp), host)
+
+
+def outer_sweep(A, f, state, schedule, P=None):
+    """GPU drop-in for richardson.outer_sweep (richardson.py:62-74): m inner
+    updates with the per-step finite check, then the residual norm appended
+    to state.residual_history.  Mutates and returns `state`."""
+    op = _op_for(A, f)
+    ds = DeviceSchedule(op, schedule, P)
+    host = _is_host(state.u)
+    u = op.to_device(state.u)
+    v = op.to_device(state.v)
+    ft = op.to_device(f)
+    ub, vb = [u.clone(), torch.empty_like(u)], [v.clone(), torch.empty_like(v)]
+    bad = torch.full((op.batch,), INT_MAX, dtype=torch.int32, device=op.device)
+    s = L.stream_ptr()
+    for i in range(ds.m):
+        L.check(op._lib.rg_inner_update(op.handle, C.byref(ds.struct), i, L.ptr(ub[i & 1]),
+                                        L.ptr(vb[i & 1]), L.ptr(ub[(i + 1) & 1]),
+                                        L.ptr(vb[(i + 1) & 1]), L.ptr(ft), L.ptr(bad), i + 1, s))
+    uf, vf = ub[ds.m & 1], vb[ds.m & 1]
+    _, n2 = op.residual(uf, ft, want_r=False)
+    first_bad = int(bad.min().item())
+    if first_bad != INT_MAX:
+        raise DivergenceError(
+            f"non-finite iterate in inner step {first_bad} of outer sweep "
+            f"{state.outer_count + 1}",
+            inner_iteration=state.outer_count * ds.m + first_bad)
+    shp = np.shape(state.u) if host else state.u.shape
+    state.u = _out(uf.reshape(shp), host)
+    state.v = _out(vf.reshape(shp), host)
+    state.outer_count += 1
+    state.residual_history.append(float(np.sqrt(n2[0].item())) if op.batch == 1
+                                  else np.sqrt(n2.cpu().numpy()))
+    return state
