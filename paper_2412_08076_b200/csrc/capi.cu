@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <string>
 #include <vector>
@@ -380,7 +381,8 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
             cudaSuccess ||
         (e = cudaMalloc((void**)&S->d_part, sizeof(double) * B * (size_t)NSLOT * cap)) !=
             cudaSuccess ||
-        (e = cudaMallocHost((void**)&S->h_st, sizeof(SysState) * B)) != cudaSuccess) {
+        !(S->h_st = (SysState*)calloc(B, sizeof(SysState)))) {
+        if (e == cudaSuccess) e = cudaErrorMemoryAllocation;
         cudaFree(S->d_st);
         cudaFree(S->d_trace);
         cudaFree(S->d_part);
@@ -396,7 +398,7 @@ int rg_solver_destroy(rg_solver* S) {
     cudaFree(S->d_st);
     cudaFree(S->d_trace);
     cudaFree(S->d_part);
-    cudaFreeHost(S->h_st);
+    free(S->h_st);
     delete S;
     return RG_OK;
 }

@@ -292,9 +292,10 @@ class GpuStencilOperator:
         t = np.zeros_like(planes)
         x, y = np.divmod(np.arange(self.P), s)
         for q, (dx, dy) in enumerate(OFFSETS9):
-            ok = (x - dx >= 0) & (x - dx < s) & (y - dy >= 0) & (y - dy < s)
+            # (A^T)[i, i+d] = A[i+d, i]: row i+d of A at offset -d (plane 8-q)
+            ok = (x + dx >= 0) & (x + dx < s) & (y + dy >= 0) & (y + dy < s)
             src = np.nonzero(ok)[0]
-            nb = (x[src] - dx) * s + (y[src] - dy)
+            nb = (x[src] + dx) * s + (y[src] + dy)
             t[:, q, src] = planes[:, 8 - q, nb]
         return GpuStencilOperator("var9", s, t, None, self.np_dtype, self.device)
 
