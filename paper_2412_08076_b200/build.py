@@ -24,8 +24,9 @@ from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
-OBJ = PKG / "build" / "obj"
-LIB = PKG / "librichgpu.so"
+OBJ = PKG / "build" / ("obj" + os.environ.get("RICHGPU_LIB_NAME", ""))
+LIB = PKG / os.environ.get("RICHGPU_LIB_NAME", "librichgpu.so")
+EXTRA = os.environ.get("RICHGPU_NVCC_FLAGS", "").split()
 INCLUDE = PKG.parent / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -47,7 +48,7 @@ def _deps_mtime() -> float:
 
 def _compile(src: Path, verbose: bool) -> tuple[Path, str]:
     obj = OBJ / (src.stem + ".o")
-    cmd = [nvcc(), *ARCH, *CFLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [nvcc(), *ARCH, *CFLAGS, *EXTRA, "-c", str(src), "-o", str(obj)]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src.name}:\n{p.stderr}")

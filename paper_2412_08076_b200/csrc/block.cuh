@@ -6,27 +6,43 @@
 // interior).  It then runs T inner steps of richardson.py:111-136 entirely
 // on chip, shrinking the valid region by one cell per step (overlapped
 // tiling), and writes back only its owned points.  HBM traffic per inner
-// step is therefore ~1/T of the unblocked sweep.
+// step is therefore ~1/T of the unblocked sweep and the kernel becomes
+// FP64-issue bound (the reference's unfused mul+add order costs 17 of the
+// ~22 FP64 instructions per point-update and cannot be contracted).
 //
 //  * The stencil input field (u for plain/mom, the look-ahead y = u + at*v
-//    for nag/nagex) lives in shared memory, ping-ponged between steps
-//    (one __syncthreads per step).
-//  * u, v, f of the thread's own points live in registers for all T steps.
+//    for nag/nagex) lives in shared memory, ping-ponged between steps (one
+//    __syncthreads per step).  For plain/mom the centre of the 3x3 window
+//    IS the thread's u, so u needs no register copy.
+//  * f (and v, and u for nag) of the thread's own points live in registers
+//    for all T steps.
+//  * Stencil coefficients and the Jacobi scale arrive as kernel parameters
+//    (uniform registers, no per-use moves).
 //  * Thread mapping: lane -> column (conflict-free 64-bit smem rows), warp
-//    -> a band of RPW rows walked with a 3x3 register window.
-//  * Each step's residual norm (the lagged convergence test, see
-//    reduce.cuh) is accumulated over the owned points and reduced by the
-//    fused epilogue.
+//    -> a band of RPW rows walked with a 3x3 register window; the CPT
+//    columns of a thread are summed interleaved for ILP.
+//  * The region bookkeeping is branch-free: values computed outside the
+//    shrinking valid region are garbage but are never read again (regions
+//    are nested), out-of-domain points are forced to 0 in shared memory,
+//    and only owned points are written back.
+//  * Each step's residual norm (the lagged convergence test, reduce.cuh) is
+//    accumulated over the owned points and reduced by the fused epilogue.
 //  * Arithmetic order is exactly the reference's (no FMA): iterates are
 //    bitwise equal to the CPU oracle.
 #pragma once
+#include <type_traits>
+
 #include "step.cuh"
 
 namespace rg {
 
+constexpr int BLK_MAXB = 64;   // systems per launch (coefficients ride in the params)
+
 template <typename S>
 struct BlockArgs {
-    const S* stencil;   // [B][9]
+    S coef[BLK_MAXB][9];   // CSR-order stencil of systems b0 .. b0+gridDim.y-1
+    S scale[BLK_MAXB];     // Jacobi scale (JAC instantiations)
+    int b0;                // first system of this launch
     int side;
     int P;
     const S* u_in;
@@ -37,7 +53,6 @@ struct BlockArgs {
     const double* omega;
     const double* alpha;
     const double* atil;
-    const S* scale;     // [B] Jacobi scale or null
     int m;
     int k0;             // global inner index of the first step of this launch
     int nty;            // tiles per system along y (columns)
@@ -46,11 +61,14 @@ struct BlockArgs {
     EpiArgs epi;
 };
 
-// Occupancy target: plain keeps u, f per point in registers (2 CTAs/SM at
-// f64); mom/nag also keep v and need the whole register file.
+// Occupancy target per (scalar, variant): registers hold f (+v, +u for nag).
+#ifndef RG_MINB_PLAIN_F64
+#define RG_MINB_PLAIN_F64 2
+#endif
 template <typename S, int VAR>
 struct BlockMinCtas {
-    static constexpr int value = (VAR == V_PLAIN) ? (sizeof(S) == 8 ? 2 : 3) : (sizeof(S) == 8 ? 1 : 2);
+    static constexpr int value = (VAR == V_PLAIN) ? (sizeof(S) == 8 ? RG_MINB_PLAIN_F64 : 3)
+                                                  : (VAR == V_MOM ? 2 : (sizeof(S) == 8 ? 1 : 2));
 };
 
 // Tile shape used by the library (load window LR x LC, NW warps).
@@ -64,9 +82,9 @@ __host__ __device__ inline int block_ntiles(int side, int T, int* nty) {
     return ntx * ny;
 }
 
-template <typename S, int VAR, int T, int LR, int LC, int NW>
+template <typename S, int VAR, int T, int LR, int LC, int NW, bool JAC>
 __global__ void __launch_bounds__(NW * 32, (BlockMinCtas<S, VAR>::value))
-block_kernel(BlockArgs<S> a) {
+block_kernel(const __grid_constant__ BlockArgs<S> a) {
     constexpr int NT = NW * 32;
     constexpr int RPW = LR / NW;   // rows per warp
     constexpr int CPT = LC / 32;   // columns per thread
@@ -76,13 +94,15 @@ block_kernel(BlockArgs<S> a) {
     constexpr bool HASV = (VAR != V_PLAIN);
     constexpr int NACC = NAG ? 1 : T;
     static_assert(LR % NW == 0 && LC % 32 == 0 && T >= 1 && TX > 0 && TY > 0, "tile");
+    static_assert(RPW * CPT <= 32, "domain mask");
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
     typedef S Row[LC];
     Row* buf0 = reinterpret_cast<Row*>(smem_raw);
     Row* buf1 = buf0 + LR;
 
-    const int b = blockIdx.y;
+    const int bl = blockIdx.y;          // system within this launch
+    const int b = a.b0 + bl;            // global system index
     if (a.epi.st[b].status != ST_ACTIVE) return;
     const int cta = blockIdx.x;
     const int ncta = gridDim.x;
@@ -95,13 +115,11 @@ block_kernel(BlockArgs<S> a) {
 
     S c[9];
 #pragma unroll
-    for (int d = 0; d < 9; ++d) c[d] = a.stencil[b * 9 + d];
-    const bool jac = (a.scale != nullptr);
-    const S sc = jac ? a.scale[b] : szero<S>();
+    for (int d = 0; d < 9; ++d) c[d] = a.coef[bl][d];
+    const S sc = JAC ? a.scale[bl] : szero<S>();
 
-    S ur[RPW][CPT], fr[RPW][CPT], vr[RPW][CPT];
+    S fr[RPW][CPT], vr[RPW][CPT], ur[RPW][CPT];
     uint32_t dom = 0;  // bit (rr*CPT+cc): point inside the interior grid
-    static_assert(RPW * CPT <= 32, "domain mask");
 
     const double at0 = NAG ? a.atil[b * a.m + (a.k0 % a.m)] : 0.0;
 #pragma unroll
@@ -113,14 +131,15 @@ block_kernel(BlockArgs<S> a) {
             const int gy = gy0 + col;
             const bool in = (gx >= 0) && (gx < side) && (gy >= 0) && (gy < side);
             const size_t g = base + (size_t)gx * side + gy;
-            ur[rr][cc] = in ? a.u_in[g] : szero<S>();
+            const S u = in ? a.u_in[g] : szero<S>();
             fr[rr][cc] = in ? a.f[g] : szero<S>();
             vr[rr][cc] = (HASV && in) ? a.v_in[g] : szero<S>();
+            if (NAG) ur[rr][cc] = u;
             if (in) dom |= 1u << (rr * CPT + cc);
-            S x = ur[rr][cc];
+            S x = u;
             if (NAG && in) x = add(x, rmul(at0, vr[rr][cc]));  // y = u + at*v
             buf0[r0 + rr][col] = x;
-            if (NAG && a.norm_first_u) buf1[r0 + rr][col] = ur[rr][cc];
+            if (NAG && a.norm_first_u) buf1[r0 + rr][col] = u;
         }
     }
     __syncthreads();
@@ -129,105 +148,127 @@ block_kernel(BlockArgs<S> a) {
 #pragma unroll
     for (int q = 0; q < NACC; ++q) acc[q] = 0.0;
 
-    // Walk the warp's row band over `src`, calling body(rr, cc, s) with the
-    // stencil sum s = A x at every point in rows [lo, hi) x cols [lo, LC-lo').
-    auto sweep_rows = [&](Row* src, int lo, int hi, int clo, int chi, auto body) {
+    // Walk the warp's row band over `src`; for every owned point call
+    // body(rr, cc, r, col, s, centre) with s = A x (CSR order, no FMA) and
+    // centre = x at the point.  The CPT column chains are interleaved.
+    auto sweep_rows = [&](Row* src, auto body) {
+        int cm[CPT], cl[CPT], cp[CPT];
 #pragma unroll
         for (int cc = 0; cc < CPT; ++cc) {
-            const int col = lane + 32 * cc;
-            const int cm = col > 0 ? col - 1 : 0;
-            const int cp = col < LC - 1 ? col + 1 : LC - 1;
-            const bool colok = (col >= clo) && (col < chi);
-            const int rm = r0 > 0 ? r0 - 1 : 0;
-            S a0 = src[rm][cm], a1 = src[rm][col], a2 = src[rm][cp];
-            S b0 = src[r0][cm], b1 = src[r0][col], b2 = src[r0][cp];
+            cl[cc] = lane + 32 * cc;
+            cm[cc] = cl[cc] > 0 ? cl[cc] - 1 : 0;
+            cp[cc] = cl[cc] < LC - 1 ? cl[cc] + 1 : LC - 1;
+        }
+        const int rm = r0 > 0 ? r0 - 1 : 0;
+        S w0[CPT], w1[CPT], w2[CPT], x0[CPT], x1[CPT], x2[CPT];
 #pragma unroll
-            for (int rr = 0; rr < RPW; ++rr) {
-                const int r = r0 + rr;
-                const int rp = r + 1 < LR ? r + 1 : LR - 1;
-                const S c0 = src[rp][cm], c1 = src[rp][col], c2 = src[rp][cp];
-                if (r >= lo && r < hi && colok) {
-                    S s = mul(c[0], a0);
-                    s = add(s, mul(c[1], a1));
-                    s = add(s, mul(c[2], a2));
-                    s = add(s, mul(c[3], b0));
-                    s = add(s, mul(c[4], b1));
-                    s = add(s, mul(c[5], b2));
-                    s = add(s, mul(c[6], c0));
-                    s = add(s, mul(c[7], c1));
-                    s = add(s, mul(c[8], c2));
-                    body(rr, cc, r, col, s);
-                }
-                a0 = b0; a1 = b1; a2 = b2;
-                b0 = c0; b1 = c1; b2 = c2;
+        for (int cc = 0; cc < CPT; ++cc) {
+            w0[cc] = src[rm][cm[cc]]; w1[cc] = src[rm][cl[cc]]; w2[cc] = src[rm][cp[cc]];
+            x0[cc] = src[r0][cm[cc]]; x1[cc] = src[r0][cl[cc]]; x2[cc] = src[r0][cp[cc]];
+        }
+#pragma unroll
+        for (int rr = 0; rr < RPW; ++rr) {
+            const int r = r0 + rr;
+            const int rp = r + 1 < LR ? r + 1 : LR - 1;
+            S y0[CPT], y1[CPT], y2[CPT], s[CPT];
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) {
+                y0[cc] = src[rp][cm[cc]]; y1[cc] = src[rp][cl[cc]]; y2[cc] = src[rp][cp[cc]];
+            }
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = mul(c[0], w0[cc]);
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[1], w1[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[2], w2[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[3], x0[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[4], x1[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[5], x2[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[6], y0[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[7], y1[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) s[cc] = add(s[cc], mul(c[8], y2[cc]));
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) {
+                body(rr, cc, r, cl[cc], s[cc], x1[cc]);
+                w0[cc] = x0[cc]; w1[cc] = x1[cc]; w2[cc] = x2[cc];
+                x0[cc] = y0[cc]; x1[cc] = y1[cc]; x2[cc] = y2[cc];
             }
         }
     };
     auto owned = [&](int r, int col) {
         return r >= T && r < LR - T && col >= T && col < LC - T;
     };
+    auto indom = [&](int rr, int cc) { return ((dom >> (rr * CPT + cc)) & 1u) != 0; };
 
     if (NAG && a.norm_first_u) {
         // residual at u itself for the sweep-boundary convergence test (:124-125)
-        sweep_rows(buf1, T, LR - T, T, LC - T, [&](int rr, int cc, int r, int col, S s) {
-            if ((dom >> (rr * CPT + cc)) & 1u) acc[0] = sqacc(acc[0], sub(fr[rr][cc], s));
+        sweep_rows(buf1, [&](int rr, int cc, int r, int col, S s, S) {
+            const S rs = (owned(r, col) && indom(rr, cc)) ? sub(fr[rr][cc], s) : szero<S>();
+            acc[0] = sqacc(acc[0], rs);
         });
         __syncthreads();
     }
 
+    // T inner steps; INTERIOR tiles (no point outside the grid, the common
+    // case) skip the domain masking entirely.
+    auto steps = [&](auto interior) {
+        constexpr bool INTERIOR = decltype(interior)::value;
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-        const int k = a.k0 + t;
-        const int si = b * a.m + (k % a.m);
-        const double w = a.omega[si];
-        const double al = HASV ? a.alpha[si] : 0.0;
-        const double atn = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
-        Row* cur = (t & 1) ? buf1 : buf0;
-        Row* nxt = (t & 1) ? buf0 : buf1;
-        const bool last = (t == T - 1);
-        sweep_rows(cur, t + 1, LR - t - 1, t + 1, LC - t - 1,
-                   [&](int rr, int cc, int r, int col, S s) {
-            S x = szero<S>();
-            if ((dom >> (rr * CPT + cc)) & 1u) {
-                const S rs = sub(fr[rr][cc], s);                       // r = f - A x
-                if (!NAG && a.norm_every && owned(r, col)) acc[(NACC > 1) ? t : 0] = sqacc(acc[(NACC > 1) ? t : 0], rs);
-                const S p = jac ? mul(sc, rs) : rs;                     // B^{-1} r
+        for (int t = 0; t < T; ++t) {
+            const int k = a.k0 + t;
+            const int si = b * a.m + (k % a.m);
+            const double w = a.omega[si];
+            const double al = HASV ? a.alpha[si] : 0.0;
+            const double atn = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+            Row* cur = (t & 1) ? buf1 : buf0;
+            Row* nxt = (t & 1) ? buf0 : buf1;
+            const bool last = (t == T - 1);
+            sweep_rows(cur, [&](int rr, int cc, int r, int col, S s, S centre) {
+                const bool live = INTERIOR || indom(rr, cc);
+                const S rs = sub(fr[rr][cc], s);                        // r = f - A x
+                if (!NAG && a.norm_every) {
+                    const S rn = (live && owned(r, col)) ? rs : szero<S>();
+                    acc[(NACC > 1) ? t : 0] = sqacc(acc[(NACC > 1) ? t : 0], rn);
+                }
+                const S p = JAC ? mul(sc, rs) : rs;                      // B^{-1} r
                 S vn;
                 if (VAR == V_PLAIN) vn = rmul(w, p);
-                else vn = add(rmul(al, vr[rr][cc]), rmul(w, p));        // v = a v + w p
-                const S un = add(ur[rr][cc], vn);                       // u = u + v
-                ur[rr][cc] = un;
+                else vn = add(rmul(al, vr[rr][cc]), rmul(w, p));         // v = a v + w p
+                const S uo = NAG ? ur[rr][cc] : centre;                  // plain/mom: x == u
+                const S un = add(uo, vn);                                // u = u + v
                 if (HASV) vr[rr][cc] = vn;
-                x = NAG ? add(un, rmul(atn, vn)) : un;
-            }
-            if (!last) nxt[r][col] = x;
-        });
-        if (!last) __syncthreads();
-    }
-
-    // write back the owned points
-#pragma unroll
-    for (int rr = 0; rr < RPW; ++rr) {
-        const int r = r0 + rr;
-        const int gx = gx0 + r;
-#pragma unroll
-        for (int cc = 0; cc < CPT; ++cc) {
-            const int col = lane + 32 * cc;
-            if (owned(r, col) && ((dom >> (rr * CPT + cc)) & 1u)) {
-                const size_t g = base + (size_t)gx * side + (gy0 + col);
-                a.u_out[g] = ur[rr][cc];
-                if (HASV) a.v_out[g] = vr[rr][cc];
-            }
+                if (NAG) ur[rr][cc] = un;
+                if (!last) {
+                    const S x = NAG ? add(un, rmul(atn, vn)) : un;       // next stencil input
+                    nxt[r][col] = live ? x : szero<S>();
+                } else if (live && owned(r, col)) {
+                    const size_t g = base + (size_t)(gx0 + r) * side + (gy0 + col);
+                    a.u_out[g] = un;
+                    if (HASV) a.v_out[g] = vn;
+                }
+            });
+            if (!last) __syncthreads();
         }
-    }
+    };
+    constexpr uint32_t FULL = (RPW * CPT == 32) ? 0xffffffffu : ((1u << (RPW * CPT)) - 1u);
+    const bool tile_inside = (gx0 >= 0) && (gy0 >= 0) && (gx0 + LR <= side) && (gy0 + LC <= side);
+    (void)FULL;
+    if (tile_inside) steps(std::integral_constant<bool, true>());
+    else steps(std::integral_constant<bool, false>());
 
     if (a.epi.nslots > 0) epilogue<NT, NACC>(a.epi, b, cta, ncta, acc, 0.0);
 }
 
-// Host launcher for one (scalar, variant): picks the T instantiation.
-template <typename S, int VAR, int T>
-cudaError_t launch_block_t(const BlockArgs<S>& a0, int batch, cudaStream_t st) {
-    auto kern = block_kernel<S, VAR, T, BLK_LR, BLK_LC, BLK_NW>;
+// Host launcher for one (scalar, variant, jacobi): picks the T instantiation.
+template <typename S, int VAR, int T, bool JAC>
+cudaError_t launch_block_t(const BlockArgs<S>& a, int nsys, cudaStream_t st) {
+    auto kern = block_kernel<S, VAR, T, BLK_LR, BLK_LC, BLK_NW, JAC>;
     const size_t smem = 2 * (size_t)BLK_LR * BLK_LC * sizeof(S);
     static bool attr_set = false;
     if (!attr_set) {
@@ -235,30 +276,36 @@ cudaError_t launch_block_t(const BlockArgs<S>& a0, int batch, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    BlockArgs<S> a = a0;
-    const int nt = block_ntiles(a.side, T, &a.nty);
-    kern<<<dim3(nt, batch), dim3(BLK_NW * 32), smem, st>>>(a);
+    const int nt = block_ntiles(a.side, T, nullptr);
+    kern<<<dim3(nt, nsys), dim3(BLK_NW * 32), smem, st>>>(a);
     return cudaGetLastError();
 }
 
-template <typename S, int VAR>
-cudaError_t launch_block(const BlockArgs<S>& a, int T, int batch, cudaStream_t st) {
+template <typename S, int VAR, bool JAC>
+cudaError_t launch_block_j(const BlockArgs<S>& a, int T, int nsys, cudaStream_t st) {
     switch (T) {
-        case 1: return launch_block_t<S, VAR, 1>(a, batch, st);
-        case 2: return launch_block_t<S, VAR, 2>(a, batch, st);
-        case 3: return launch_block_t<S, VAR, 3>(a, batch, st);
-        case 4: return launch_block_t<S, VAR, 4>(a, batch, st);
-        case 5: return launch_block_t<S, VAR, 5>(a, batch, st);
-        case 6: return launch_block_t<S, VAR, 6>(a, batch, st);
-        case 7: return launch_block_t<S, VAR, 7>(a, batch, st);
-        case 8: return launch_block_t<S, VAR, 8>(a, batch, st);
+        case 1: return launch_block_t<S, VAR, 1, JAC>(a, nsys, st);
+        case 2: return launch_block_t<S, VAR, 2, JAC>(a, nsys, st);
+        case 3: return launch_block_t<S, VAR, 3, JAC>(a, nsys, st);
+        case 4: return launch_block_t<S, VAR, 4, JAC>(a, nsys, st);
+        case 5: return launch_block_t<S, VAR, 5, JAC>(a, nsys, st);
+        case 6: return launch_block_t<S, VAR, 6, JAC>(a, nsys, st);
+        case 7: return launch_block_t<S, VAR, 7, JAC>(a, nsys, st);
+        case 8: return launch_block_t<S, VAR, 8, JAC>(a, nsys, st);
     }
     return cudaErrorInvalidValue;
 }
 
+// a.nty must be set by the caller (block_ntiles(side, T, &nty)).
+template <typename S, int VAR>
+cudaError_t launch_block(const BlockArgs<S>& a, int T, bool jac, int nsys, cudaStream_t st) {
+    return jac ? launch_block_j<S, VAR, true>(a, T, nsys, st)
+               : launch_block_j<S, VAR, false>(a, T, nsys, st);
+}
+
 // Explicit instantiations live in block_<dtype>_<variant>.cu (parallel build).
 #define RG_DECLARE_BLOCK(S, VAR) \
-    extern template cudaError_t launch_block<S, VAR>(const BlockArgs<S>&, int, int, cudaStream_t);
+    extern template cudaError_t launch_block<S, VAR>(const BlockArgs<S>&, int, bool, int, cudaStream_t);
 RG_DECLARE_BLOCK(double, V_PLAIN)
 RG_DECLARE_BLOCK(double, V_MOM)
 RG_DECLARE_BLOCK(double, V_NAG)

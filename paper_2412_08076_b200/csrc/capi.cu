@@ -47,6 +47,7 @@ static int fail(int code, const char* fmt, ...) {
 struct rg_op {
     rg_op_desc d;
     int P;
+    std::vector<double> hcoef;   // CONST9 real: host copy of [batch][9] (kernel params)
 };
 
 struct rg_solver {
@@ -65,6 +66,7 @@ struct rg_solver {
     void* u[2];
     void* v[2];
     const void* f;
+    std::vector<double> hscale;   // Jacobi scale per system (blocked path)
     long long k;
     long long kmax;
     long long flushed_k;
@@ -165,8 +167,7 @@ static int step1(const rg_op* A, const StepReq& q, cudaStream_t st) {
 template <typename S>
 static int do_block(rg_solver* S_, int T, int norm_first_u, cudaStream_t st) {
     const rg_op* A = S_->A;
-    BlockArgs<S> a;
-    a.stencil = (const S*)A->d.stencil;
+    static thread_local BlockArgs<S> a;   // ~5 KB of kernel parameters
     a.side = A->d.side;
     a.P = A->P;
     a.u_in = (const S*)S_->u[S_->cur];
@@ -177,12 +178,13 @@ static int do_block(rg_solver* S_, int T, int norm_first_u, cudaStream_t st) {
     a.omega = S_->s.omega;
     a.alpha = S_->s.alpha;
     a.atil = S_->s.alpha_tilde;
-    a.scale = S_->s.precond == RG_PRECOND_JACOBI_SCALAR ? (const S*)S_->s.scale : nullptr;
     a.m = S_->s.m;
     a.k0 = (int)S_->k;
     const bool nag = S_->s.variant >= RG_NAG;
+    const bool jac = S_->s.precond == RG_PRECOND_JACOBI_SCALAR;
     a.norm_first_u = norm_first_u;
     a.norm_every = nag ? 0 : 1;
+    block_ntiles(A->d.side, T, &a.nty);
     EpiArgs& e = a.epi;
     e.st = S_->d_st;
     e.trace = S_->d_trace;
@@ -194,13 +196,22 @@ static int do_block(rg_solver* S_, int T, int norm_first_u, cudaStream_t st) {
     e.nslots = nag ? (norm_first_u ? 1 : 0) : T;
     e.with_f = 0;
     e.buf = S_->cur;
-    cudaError_t err;
-    switch (S_->s.variant) {
-        case RG_PLAIN: err = launch_block<S, V_PLAIN>(a, T, A->d.batch, st); break;
-        case RG_MOM: err = launch_block<S, V_MOM>(a, T, A->d.batch, st); break;
-        default: err = launch_block<S, V_NAG>(a, T, A->d.batch, st); break;
+    const int B = A->d.batch;
+    for (int b0 = 0; b0 < B; b0 += BLK_MAXB) {
+        const int nsys = B - b0 < BLK_MAXB ? B - b0 : BLK_MAXB;
+        a.b0 = b0;
+        for (int j = 0; j < nsys; ++j) {
+            for (int d = 0; d < 9; ++d) a.coef[j][d] = (S)A->hcoef[(size_t)(b0 + j) * 9 + d];
+            a.scale[j] = jac ? (S)S_->hscale[b0 + j] : (S)0;
+        }
+        cudaError_t err;
+        switch (S_->s.variant) {
+            case RG_PLAIN: err = launch_block<S, V_PLAIN>(a, T, jac, nsys, st); break;
+            case RG_MOM: err = launch_block<S, V_MOM>(a, T, jac, nsys, st); break;
+            default: err = launch_block<S, V_NAG>(a, T, jac, nsys, st); break;
+        }
+        if (err != cudaSuccess) return fail(RG_ECUDA, "block sweep launch: %s", cudaGetErrorString(err));
     }
-    if (err != cudaSuccess) return fail(RG_ECUDA, "block sweep launch: %s", cudaGetErrorString(err));
     return RG_OK;
 }
 
@@ -245,6 +256,23 @@ int rg_op_create(rg_op** out, const rg_op_desc* d) {
     rg_op* A = new rg_op;
     A->d = *d;
     A->P = d->side * d->side;
+    if (d->kind == RG_CONST9 && (d->dtype == RG_F64 || d->dtype == RG_F32)) {
+        // the blocked sweep takes the 9 coefficients as kernel parameters
+        const size_t n = (size_t)d->batch * 9;
+        A->hcoef.resize(n);
+        cudaError_t e;
+        if (d->dtype == RG_F64) {
+            e = cudaMemcpy(A->hcoef.data(), d->stencil, n * sizeof(double), cudaMemcpyDeviceToHost);
+        } else {
+            std::vector<float> tmp(n);
+            e = cudaMemcpy(tmp.data(), d->stencil, n * sizeof(float), cudaMemcpyDeviceToHost);
+            for (size_t i = 0; i < n; ++i) A->hcoef[i] = tmp[i];
+        }
+        if (e != cudaSuccess) {
+            delete A;
+            return fail(RG_ECUDA, "reading CONST9 coefficients: %s", cudaGetErrorString(e));
+        }
+    }
     *out = A;
     return RG_OK;
 }
@@ -350,8 +378,7 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     if (max_outer < 0) return fail(RG_EINVAL, "max_outer must be >= 0");
     if ((long long)max_outer * s->m > 2000000000ll) return fail(RG_ESIZE, "max_outer*m too large");
     if (block_T < 0 || block_T > 8) return fail(RG_EINVAL, "block_T must be in [0, 8]");
-    rg_solver* S = new rg_solver;
-    memset(S, 0, sizeof *S);
+    rg_solver* S = new rg_solver();
     S->A = A;
     S->s = *s;
     S->cfg.tol = tol;
@@ -363,7 +390,8 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     const bool real = A->d.dtype == RG_F32 || A->d.dtype == RG_F64;
     S->use_block = real && A->d.kind == RG_CONST9 && check == RG_CHECK_OUTER &&
                    s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
-    S->block_T = block_T == 0 ? 4 : block_T;
+    // automatic depth: measured optimum on B200 for the 64x64 tile (profiles/)
+    S->block_T = block_T != 0 ? block_T : (s->variant >= RG_NAG ? 6 : 5);
     if (!S->use_block) S->block_T = 1;
     S->kmax = (long long)max_outer * s->m;
     const dim3 g = step_grid(A);
@@ -436,6 +464,22 @@ int rg_solver_begin(rg_solver* S, void* u0, void* u1, void* v0, void* v1, const 
     S->launches = 0;
     S->flushed_k = 0;
     S->need_flush = false;
+    if (S->use_block && S->s.precond == RG_PRECOND_JACOBI_SCALAR) {
+        // the blocked sweep takes the per-system Jacobi scale as a kernel parameter
+        const int B = A->d.batch;
+        S->hscale.resize(B);
+        if (A->d.dtype == RG_F64) {
+            CUDA_TRY(cudaMemcpyAsync(S->hscale.data(), S->s.scale, B * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+        } else {
+            std::vector<float> tmp(B);
+            CUDA_TRY(cudaMemcpyAsync(tmp.data(), S->s.scale, B * sizeof(float),
+                                     cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            for (int b = 0; b < B; ++b) S->hscale[b] = tmp[b];
+        }
+    }
     CUDA_TRY(cudaMemsetAsync(S->d_st, 0, sizeof(SysState) * A->d.batch, st));
     CUDA_TRY(cudaMemsetAsync(S->d_trace, 0, sizeof(double) * A->d.batch * (size_t)S->trace_stride, st));
     if (v0) CUDA_TRY(cudaMemsetAsync(v0, 0, vbytes, st));  // v = 0 at entry (:95)

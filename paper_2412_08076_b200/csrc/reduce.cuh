@@ -111,15 +111,15 @@ __device__ void epilogue(const EpiArgs& e, int b, int cta, int ncta,
         const double s = block_sum<NT>(facc, red);
         if (tid == 0) part[(NSLOT - 1) * e.ncta_cap + cta] = s;
     }
-    __threadfence();
-    __syncthreads();
+    // only thread 0 wrote partials: it alone fences before taking a ticket
     if (tid == 0) {
+        __threadfence();
         const int t = atomicAdd(&e.st[b].counter, 1);
         is_last = (t == ncta - 1);
+        if (is_last) __threadfence();
     }
     __syncthreads();
     if (!is_last) return;
-    __threadfence();
     __shared__ double tot[NSLOT];
     for (int q = 0; q < NSLOT; ++q) {
         const bool want = (q < e.nslots) || (q == NSLOT - 1 && e.with_f);
