@@ -131,6 +131,31 @@ int rg_inner_update(const rg_op* A, const rg_sched* s, int i,
                     void* u_out, void* v_out, const void* f,
                     int* nonfinite_at, int tag, void* stream);
 
+/* n_steps free-running inner updates (schedule index (i0 + t) mod m), with
+ * no residual norms and no status: the smoothing loops of fns_lite_step
+ * (fns.py:78-79, plain, weights cycled) and multigrid._smooth
+ * (multigrid.py:126-138, fresh v, no preconditioner).  u0 holds the input
+ * (and v0 the input velocity); u0/u1, v0/v1 are ping-pong buffers and
+ * *out_buf (host int) says which one holds the result.  block_T as for the
+ * solver (CONST9 real operators run temporally blocked). */
+int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T,
+             void* u0, void* u1, void* v0, void* v1, const void* f, int* out_buf,
+             void* stream);
+
+/* ---- DST-I / FNS correction (transforms.py:24-35, fns.py:30-84) ----------
+ * A plan holds the twiddle table and one [batch][side][side] workspace; one
+ * call in flight per plan.  side+1 must be a power of two (4 .. 8192). */
+typedef struct rg_dst rg_dst;
+int rg_dst_create(rg_dst** out, int batch, int side);
+int rg_dst_destroy(rg_dst* plan);
+/* out = dst2(in) for every system (orthonormal 2D DST-I, involutory);
+ * in and out may alias.  float64. */
+int rg_dst2(const rg_dst* plan, const double* in, double* out, void* stream);
+/* u += dst2(lam * dst2(f - A u)) for every system (SpectralCorrection.apply,
+ * fns.py:43-44,80); lam is [batch][side*side] float64. */
+int rg_fns_correct(const rg_op* A, const rg_dst* plan, const double* lam, double* u,
+                   const double* f, void* stream);
+
 /* ---- solve_stationary engine (richardson.py:77-141) ----------------------
  * A solver owns device workspace (per-system status, trace, reduction
  * partials) and runs the whole loop on the device: convergence, divergence

@@ -52,6 +52,11 @@ _SIGS = [
     ("rg_matvec", _I, [_P, _P, _P, _P]),
     ("rg_residual", _I, [_P, _P, _P, _P, _P, _P]),
     ("rg_inner_update", _I, [_P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P, _P, _I, _P]),
+    ("rg_sweep", _I, [_P, C.POINTER(rg_sched), _I, _I, _I, _P, _P, _P, _P, _P, C.POINTER(_I), _P]),
+    ("rg_dst_create", _I, [C.POINTER(_P), _I, _I]),
+    ("rg_dst_destroy", _I, [_P]),
+    ("rg_dst2", _I, [_P, _P, _P, _P]),
+    ("rg_fns_correct", _I, [_P, _P, _P, _P, _P, _P]),
     ("rg_solver_create", _I, [C.POINTER(_P), _P, C.POINTER(rg_sched), C.c_double, _I, _I, _I]),
     ("rg_solver_destroy", _I, [_P]),
     ("rg_solver_begin", _I, [_P, _P, _P, _P, _P, _P, _P]),
@@ -106,6 +111,9 @@ def check(rc):
             raise DimensionMismatch(msg)
         if rc in (RG_EINVAL,):
             raise ValueError(msg)
+        if rc == RG_EUNSUPPORTED:
+            from .errors import UnsupportedOperator
+            raise UnsupportedOperator(msg)
         raise RichGpuError(rc, msg)
     return rc
 

@@ -103,7 +103,7 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
 
     const int bl = blockIdx.y;          // system within this launch
     const int b = a.b0 + bl;            // global system index
-    if (a.epi.st[b].status != ST_ACTIVE) return;
+    if (a.epi.st && a.epi.st[b].status != ST_ACTIVE) return;   // st == null: free-running sweep
     const int cta = blockIdx.x;
     const int ncta = gridDim.x;
     const int tx = cta / a.nty, ty = cta - (cta / a.nty) * a.nty;

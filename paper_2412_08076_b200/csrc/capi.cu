@@ -13,6 +13,7 @@
 
 #include "../../include/richgpu.h"
 #include "block.cuh"
+#include "dst.cuh"
 
 using namespace rg;
 
@@ -236,6 +237,80 @@ static int check_sched(const rg_op* A, const rg_sched* s) {
     return RG_OK;
 }
 
+struct rg_dst {
+    int batch, side, M, logM, lpc;
+    double2* tw;     // [M]
+    double* work;    // [batch][side][side] residual / intermediate
+};
+
+static int dst_pass(const rg_dst* D, int axis, int mode, const double* in, double* out,
+                    const double* lam, cudaStream_t st) {
+    DstArgs a;
+    a.in = in;
+    a.out = out;
+    a.tw = D->tw;
+    a.lam = lam;
+    a.N = D->side;
+    a.M = D->M;
+    a.logM = D->logM;
+    a.lpc = D->lpc;
+    a.mode = mode;
+    a.scale = sqrt(2.0 / D->M);
+    const size_t smem = (size_t)D->lpc * (D->M * sizeof(double2) +
+                                          (mode == DST_TWICE_LAM ? D->side * sizeof(double) : 0));
+    const dim3 grid((D->side + D->lpc - 1) / D->lpc, D->batch);
+    if (axis == 0) {
+        CUDA_TRY(cudaFuncSetAttribute(dst_lines_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dst_lines_kernel<0><<<grid, DST_NT, smem, st>>>(a);
+    } else {
+        CUDA_TRY(cudaFuncSetAttribute(dst_lines_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dst_lines_kernel<1><<<grid, DST_NT, smem, st>>>(a);
+    }
+    LAUNCH_CHECK();
+    return RG_OK;
+}
+
+// Free-running inner steps (no norms, no status): see rg_sweep in the header.
+template <typename S>
+static int sweep_block(const rg_op* A, const rg_sched* s, int k0, int T, bool jac_scalar,
+                       const std::vector<double>& hscale, void* uin, void* uout, void* vin,
+                       void* vout, const void* f, cudaStream_t st) {
+    static thread_local BlockArgs<S> a;
+    memset(&a.epi, 0, sizeof a.epi);
+    a.side = A->d.side;
+    a.P = A->P;
+    a.u_in = (const S*)uin;
+    a.u_out = (S*)uout;
+    a.v_in = (const S*)vin;
+    a.v_out = (S*)vout;
+    a.f = (const S*)f;
+    a.omega = s->omega;
+    a.alpha = s->alpha;
+    a.atil = s->alpha_tilde;
+    a.m = s->m;
+    a.k0 = k0;
+    a.norm_first_u = 0;
+    a.norm_every = 0;
+    block_ntiles(A->d.side, T, &a.nty);
+    const int B = A->d.batch;
+    for (int b0 = 0; b0 < B; b0 += BLK_MAXB) {
+        const int nsys = B - b0 < BLK_MAXB ? B - b0 : BLK_MAXB;
+        a.b0 = b0;
+        for (int j = 0; j < nsys; ++j) {
+            for (int d = 0; d < 9; ++d) a.coef[j][d] = (S)A->hcoef[(size_t)(b0 + j) * 9 + d];
+            a.scale[j] = jac_scalar ? (S)hscale[b0 + j] : (S)0;
+        }
+        cudaError_t err;
+        switch (s->variant) {
+            case RG_PLAIN: err = launch_block<S, V_PLAIN>(a, T, jac_scalar, nsys, st); break;
+            case RG_MOM: err = launch_block<S, V_MOM>(a, T, jac_scalar, nsys, st); break;
+            default: err = launch_block<S, V_NAG>(a, T, jac_scalar, nsys, st); break;
+        }
+        if (err != cudaSuccess) return fail(RG_ECUDA, "sweep launch: %s", cudaGetErrorString(err));
+    }
+    return RG_OK;
+}
+
 // ==================================================================== C ABI
 extern "C" {
 
@@ -364,6 +439,142 @@ int rg_inner_update(const rg_op* A, const rg_sched* s, int i, const void* u_in, 
     q.nonfinite_at = nonfinite_at;
     q.tag = tag;
     return step1(A, q, (cudaStream_t)stream);
+}
+
+int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,
+             void* u1, void* v0, void* v1, const void* f, int* out_buf, void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if ((rc = check_sched(A, s))) return rc;
+    if (!u0 || !u1 || !f || !out_buf) return fail(RG_ENULL, "null argument");
+    if (s->variant != RG_PLAIN && (!v0 || !v1)) return fail(RG_ENULL, "variant needs v0/v1");
+    if (n_steps < 0 || i0 < 0) return fail(RG_EINVAL, "negative step count or index");
+    if (block_T < 0 || block_T > 8) return fail(RG_EINVAL, "block_T must be in [0, 8]");
+    cudaStream_t st = (cudaStream_t)stream;
+    void* u[2] = {u0, u1};
+    void* v[2] = {v0, v1};
+    int cur = 0;
+    const bool real = A->d.dtype == RG_F32 || A->d.dtype == RG_F64;
+    const bool blocked = real && A->d.kind == RG_CONST9 &&
+                         s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
+    std::vector<double> hscale;
+    const bool jac = s->precond == RG_PRECOND_JACOBI_SCALAR;
+    if (blocked && jac) {
+        const int B = A->d.batch;
+        hscale.resize(B);
+        if (A->d.dtype == RG_F64) {
+            CUDA_TRY(cudaMemcpyAsync(hscale.data(), s->scale, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+        } else {
+            std::vector<float> tmp(B);
+            CUDA_TRY(cudaMemcpyAsync(tmp.data(), s->scale, B * sizeof(float), cudaMemcpyDeviceToHost, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+            for (int b = 0; b < B; ++b) hscale[b] = tmp[b];
+        }
+    }
+    const int T = block_T == 0 ? (s->variant >= RG_NAG ? 6 : 5) : block_T;
+    int k = i0;
+    int left = n_steps;
+    while (left > 0) {
+        const int t = blocked ? (T < left ? T : left) : 1;
+        if (blocked) {
+            rc = A->d.dtype == RG_F64
+                     ? sweep_block<double>(A, s, k, t, jac, hscale, u[cur], u[cur ^ 1], v[cur], v[cur ^ 1], f, st)
+                     : sweep_block<float>(A, s, k, t, jac, hscale, u[cur], u[cur ^ 1], v[cur], v[cur ^ 1], f, st);
+        } else {
+            StepReq q;
+            memset(&q, 0, sizeof q);
+            q.u_in = u[cur];
+            q.u_out = u[cur ^ 1];
+            q.v_in = v[cur];
+            q.v_out = v[cur ^ 1];
+            q.f = f;
+            q.omega = s->omega;
+            q.alpha = s->alpha;
+            q.atil = s->alpha_tilde;
+            q.scale = s->scale;
+            q.m = s->m;
+            q.i = k % s->m;
+            q.variant = s->variant;
+            q.precond = s->precond;
+            q.update = 1;
+            rc = step1(A, q, st);
+        }
+        if (rc) return rc;
+        cur ^= 1;
+        k += t;
+        left -= t;
+    }
+    *out_buf = cur;
+    return RG_OK;
+}
+
+int rg_dst_create(rg_dst** out, int batch, int side) {
+    if (!out) return fail(RG_ENULL, "null out");
+    const int M = side + 1;
+    if (batch < 1 || side < 3 || (M & (M - 1)) != 0 || M > 8192)
+        return fail(RG_EUNSUPPORTED, "DST needs side+1 a power of two in [4, 8192] (got side=%d)", side);
+    rg_dst* D = new rg_dst();
+    D->batch = batch;
+    D->side = side;
+    D->M = M;
+    D->logM = 0;
+    while ((1 << D->logM) < M) ++D->logM;
+    int lpc = 4096 / M;
+    D->lpc = lpc < 1 ? 1 : (lpc > 8 ? 8 : lpc);
+    std::vector<double2> tw(M);
+    for (int k = 0; k < M; ++k) {
+        // (cos, sin)(pi k / M), symmetric evaluation for accuracy
+        const double ang = M_PI * (double)k / (double)M;
+        tw[k] = make_double2(cos(ang), sin(ang));
+    }
+    cudaError_t e;
+    if ((e = cudaMalloc((void**)&D->tw, sizeof(double2) * M)) != cudaSuccess ||
+        (e = cudaMalloc((void**)&D->work, sizeof(double) * (size_t)batch * side * side)) != cudaSuccess ||
+        (e = cudaMemcpy(D->tw, tw.data(), sizeof(double2) * M, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        cudaFree(D->tw);
+        cudaFree(D->work);
+        delete D;
+        return fail(RG_ECUDA, "dst plan: %s", cudaGetErrorString(e));
+    }
+    *out = D;
+    return RG_OK;
+}
+
+int rg_dst_destroy(rg_dst* D) {
+    if (!D) return RG_OK;
+    cudaFree(D->tw);
+    cudaFree(D->work);
+    delete D;
+    return RG_OK;
+}
+
+int rg_dst2(const rg_dst* D, const double* in, double* out, void* stream) {
+    if (!D || !in || !out) return fail(RG_ENULL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    int rc = dst_pass(D, 0, DST_PLAIN, in, out, nullptr, st);
+    if (rc) return rc;
+    return dst_pass(D, 1, DST_PLAIN, out, out, nullptr, st);
+}
+
+int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u, const double* f,
+                   void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if (!D || !lam || !u || !f) return fail(RG_ENULL, "null argument");
+    if (A->d.dtype != RG_F64) return fail(RG_EUNSUPPORTED, "FNS correction is float64 (fns.py:36)");
+    if (A->d.side != D->side || A->d.batch != D->batch) return fail(RG_ESIZE, "plan/operator shape mismatch");
+    cudaStream_t st = (cudaStream_t)stream;
+    StepReq q;
+    memset(&q, 0, sizeof q);
+    q.u_in = u;
+    q.f = f;
+    q.r_out = D->work;   // r = f - A u
+    q.m = 1;
+    if ((rc = step1(A, q, st))) return rc;
+    if ((rc = dst_pass(D, 0, DST_PLAIN, D->work, D->work, nullptr, st))) return rc;
+    if ((rc = dst_pass(D, 1, DST_TWICE_LAM, D->work, D->work, lam, st))) return rc;
+    return dst_pass(D, 0, DST_ADD, D->work, u, nullptr, st);
 }
 
 int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double tol,

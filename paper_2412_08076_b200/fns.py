@@ -1,0 +1,189 @@
+"""GPU drop-in for the FNS-lite hybrid iteration (fns.py:30-105) and the
+orthonormal 2D DST-I (transforms.py:24-35).
+
+    dst2(x) / dst2_inv(x)                          -> like x
+    SpectralCorrection(lambda_tilde, n)            (.apply(r))
+    fns_lite_step(A, f, u, schedule, M, corr)      -> u
+    solve_fns(A, f, schedule, corr, M, tol, max_iters) -> (u, SolveReport)
+
+The M smoothing steps run as one temporally blocked sweep (plain Richardson,
+weights cycled mod m, no preconditioner); the correction is one residual
+kernel plus three shared-memory DST line passes (rows; columns with the
+symbol multiply between two transforms; rows accumulated into u).  The DST
+is not bitwise pocketfft: agreement ~1e-15 relative.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .errors import DivergenceError, SolveReport
+from .operator import GpuStencilOperator
+from .richardson import DeviceSchedule, _is_host, _op_for
+
+_PLANS = {}
+
+
+def dst_plan(batch, side):
+    """Cached rg_dst plan (twiddles + workspace) for (batch, side)."""
+    key = (batch, side, torch.cuda.current_device())
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = _DstPlan(batch, side)
+        _PLANS[key] = plan
+    return plan
+
+
+class _DstPlan:
+    def __init__(self, batch, side):
+        self.lib = L.load()
+        h = C.c_void_p()
+        L.check(self.lib.rg_dst_create(C.byref(h), int(batch), int(side)))
+        self.h, self.batch, self.side = h, batch, side
+
+    def __del__(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.rg_dst_destroy(self.h)
+            self.h = None
+
+
+def _as_grid_batch(x):
+    """(device float64 tensor [B, s*s], batch, side, host?)"""
+    host = _is_host(x)
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, dtype=np.float64))
+    t = t.to(device="cuda", dtype=torch.float64)
+    n = t.shape[-1] if t.ndim >= 1 else t.numel()
+    side = math.isqrt(n)
+    if side * side != n:
+        raise ValueError(f"vector length {n} is not a perfect square")
+    return t.reshape(-1, n).contiguous(), t.numel() // n, side, host
+
+
+def dst2(x):
+    """Orthonormal 2D DST-I of flattened interior vector(s) (transforms.py:24-30)."""
+    t, B, side, host = _as_grid_batch(x)
+    out = torch.empty_like(t)
+    L.check(dst_plan(B, side).lib.rg_dst2(dst_plan(B, side).h, L.ptr(t), L.ptr(out),
+                                          L.stream_ptr()))
+    out = out.reshape(np.shape(x) if host else x.shape)
+    return out.cpu().numpy() if host else out
+
+
+def dst2_inv(x):
+    """transforms.py:33-35 (the transform is involutory)."""
+    return dst2(x)
+
+
+class SpectralCorrection:
+    """Diagonal operator in the sine basis (fns.py:30-44); the symbol lives
+    on the device.  lambda_tilde: [(n-1)^2] or a batch [B, (n-1)^2]."""
+
+    def __init__(self, lambda_tilde, n):
+        lam = lambda_tilde if isinstance(lambda_tilde, torch.Tensor) else torch.as_tensor(
+            np.asarray(lambda_tilde, dtype=np.float64))
+        lam = lam.to(device="cuda", dtype=torch.float64)
+        if lam.shape[-1] != (n - 1) ** 2:
+            raise ValueError("correction length does not match the grid")
+        if not bool(torch.isfinite(lam).all()):
+            raise ValueError("correction entries must be finite")
+        self.lam = lam.reshape(-1, (n - 1) ** 2).contiguous()
+        self.n = n
+        self.lambda_tilde = lambda_tilde
+
+    def apply(self, r):
+        return dst2_inv(self._times(dst2(r)))
+
+    def _times(self, x):
+        host = not isinstance(x, torch.Tensor)
+        t = torch.as_tensor(x).to("cuda", torch.float64).reshape(self.lam.shape)
+        y = (t * self.lam).reshape(np.shape(x) if host else x.shape)
+        return y.cpu().numpy() if host else y
+
+
+class FnsEngine:
+    """Device state of the hybrid iteration for a batch of systems."""
+
+    def __init__(self, op: GpuStencilOperator, schedule, corr: SpectralCorrection, M):
+        if op.np_dtype != np.float64:
+            raise ValueError("FNS runs in float64 (fns.py:36)")
+        self.op, self.M = op, int(M)
+        self.sched = DeviceSchedule(op, schedule, None)
+        if self.sched.variant != "plain":
+            # fns_lite_step uses omega only (fns.py:78-79)
+            from .schedules import WeightSchedule
+            self.sched = DeviceSchedule(op, WeightSchedule(omega=np.asarray(schedule.omega)), None)
+        lam = corr.lam
+        if lam.shape[0] == 1 and op.batch > 1:
+            lam = lam.expand(op.batch, -1).contiguous()
+        if lam.shape[0] != op.batch:
+            raise ValueError("one symbol per system (or one shared) expected")
+        self.lam = lam
+        self.plan = dst_plan(op.batch, op.side)
+        self.u = [torch.empty((op.batch, op.P), dtype=torch.float64, device=op.device)
+                  for _ in range(2)]
+        self.cur = 0
+
+    def step(self, f):
+        """fns_lite_step on the device iterate self.u[self.cur] (no host sync)."""
+        lib = self.op._lib
+        outb = C.c_int()
+        if self.M > 0:
+            L.check(lib.rg_sweep(self.op.handle, C.byref(self.sched.struct), 0, self.M, 0,
+                                 L.ptr(self.u[self.cur]), L.ptr(self.u[self.cur ^ 1]), None, None,
+                                 L.ptr(f), C.byref(outb), L.stream_ptr()))
+            self.cur = self.cur ^ outb.value
+        L.check(lib.rg_fns_correct(self.op.handle, self.plan.h, L.ptr(self.lam),
+                                   L.ptr(self.u[self.cur]), L.ptr(f), L.stream_ptr()))
+        return self.u[self.cur]
+
+
+def fns_lite_step(A, f, u, schedule, M, corr: SpectralCorrection):
+    """fns.py:76-84: M plain smoothing steps (omega[k % m]), one correction,
+    non-finite check.  Returns u like the input."""
+    op = _op_for(A, f)
+    eng = FnsEngine(op, schedule, corr, M)
+    host = _is_host(u)
+    ft = op.to_device(f)
+    eng.u[0].copy_(op.to_device(u))
+    out = eng.step(ft)
+    if not bool(torch.isfinite(out).all()):
+        raise DivergenceError("hybrid step produced a non-finite iterate", inner_iteration=M)
+    shp = np.shape(u) if host else u.shape
+    out = out.reshape(shp)
+    return out.cpu().numpy() if host else out.clone()
+
+
+def solve_fns(A, f, schedule, corr, M, tol=1e-6, max_iters=10_000):
+    """fns.py:87-105 on the device: hybrid steps from zero until the relative
+    residual (one fused residual-norm per step, host-polled) reaches tol."""
+    t0 = time.perf_counter()
+    op = _op_for(A, f)
+    host = _is_host(f)
+    ft = op.to_device(f)
+    eng = FnsEngine(op, schedule, corr, M)
+    eng.u[0].zero_()
+    fn2 = torch.linalg.vector_norm(ft, dim=1)
+    fnorm = float(fn2[0].item()) if op.batch == 1 else fn2.cpu().numpy()
+    if op.batch != 1:
+        raise ValueError("solve_fns drives one system; use FnsEngine for batches")
+    rel, trace, it = 1.0, [1.0], 0
+    converged = fnorm == 0.0
+    while not converged and it < max_iters:
+        u = eng.step(ft)
+        it += 1
+        _, n2 = op.residual(u, ft, want_r=False)
+        r2 = float(n2[0].item())
+        if not math.isfinite(r2):
+            raise DivergenceError("hybrid step produced a non-finite iterate", inner_iteration=M)
+        rel = math.sqrt(r2) / fnorm
+        trace.append(rel)
+        converged = rel <= tol
+    u = eng.u[eng.cur].reshape(-1)
+    return (u.cpu().numpy() if host else u.clone()), SolveReport(
+        iterations=it, inner_iterations=it * M, converged=converged,
+        final_relative_residual=rel, wall_time=time.perf_counter() - t0, trace=np.array(trace))

@@ -1,0 +1,104 @@
+"""FNS-lite (cfg 4 path): GPU DST-I and hybrid step vs the reference goldens.
+The DST is an FFT, not pocketfft's: tolerance 1e-12 relative."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import paper_2412_08076_b200 as G
+from paper_2412_08076_b200 import fns as GF
+
+pytestmark = pytest.mark.gpu
+RTOL = 1e-12
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b)
+
+
+def test_dst2_golden(golden):
+    d = golden("fns")
+    assert _rel(GF.dst2(d["x31"]), d["d31"]) <= 1e-14
+    assert _rel(GF.dst2(d["x63"]), d["d63"]) <= 1e-14
+
+
+@pytest.mark.parametrize("side", [3, 7, 15, 255, 1023])
+def test_dst2_vs_scipy_and_involution(side):
+    rng = np.random.default_rng(side)
+    x = rng.standard_normal((2, side * side))
+    y = GF.dst2(x)
+    for b in range(2):
+        assert _rel(y[b], O.dst2(x[b])) <= 1e-13
+    z = GF.dst2(y)
+    assert _rel(z, x) <= 1e-13                       # involutory (transforms.py:33-35)
+    assert abs(np.linalg.norm(y) / np.linalg.norm(x) - 1) <= 1e-13   # orthonormal
+
+
+def test_sine_mode_is_unit_coefficient():
+    """transforms.py:38-43 / test_transforms.py analogue."""
+    n = 32
+    i = np.arange(1, n)
+    mode = np.outer(np.sin(3 * np.pi * i / n), np.sin(5 * np.pi * i / n)).reshape(-1)
+    c = GF.dst2(mode)
+    k = np.argmax(np.abs(c))
+    assert k == 2 * (n - 1) + 4
+    assert np.allclose(np.delete(c, k), 0, atol=1e-12)
+
+
+def test_fns_step_and_solve_golden(golden):
+    d = golden("fns")
+    n = int(d["n"])
+    A = O.assemble_anisotropic(float(d["eps"]), float(d["theta"]), n)
+    corr = GF.SpectralCorrection(d["lam"], n)
+    sch = G.WeightSchedule(omega=np.full(8, 0.5))
+    u1 = GF.fns_lite_step(A, d["f"], np.zeros(A.shape[0]), sch, 8, corr)
+    assert _rel(u1, d["u1"]) <= RTOL
+    u, rep = GF.solve_fns(A, d["f"], sch, corr, 8, tol=1e-300, max_iters=5)
+    assert rep.iterations == 5 and rep.inner_iterations == 40
+    assert _rel(u, d["u5"]) <= RTOL
+    assert np.all(np.abs(rep.trace - d["trace5"]) <= RTOL * d["trace5"])
+
+
+def test_exact_inverse_correction(golden):
+    """test_fns.py:31-40 / acceptance criterion 6: eps=1 operator, lambda =
+    1/eigenvalue, zero smoothing -> one step solves the system."""
+    d = golden("fns")
+    A1 = O.assemble_anisotropic(1.0, 0.0, 16)
+    u = GF.fns_lite_step(A1, d["f1"], np.zeros(A1.shape[0]), G.WeightSchedule(omega=[0.0]), 0,
+                         GF.SpectralCorrection(d["lam1"], 16))
+    assert _rel(u, d["u_exact"]) <= RTOL
+    assert np.linalg.norm(d["f1"] - A1.dot(u)) <= 1e-12 * np.linalg.norm(d["f1"])
+
+
+def test_lambda_zero_is_pure_smoothing():
+    """test_fns.py:18-28: lambda = 0 reduces the step to M Richardson steps."""
+    A = O.assemble_anisotropic(0.1, 0.7, 32)
+    f = np.random.default_rng(1).standard_normal(A.shape[0])
+    u = GF.fns_lite_step(A, f, np.zeros(A.shape[0]), G.WeightSchedule(omega=[0.3, 0.5]), 5,
+                         GF.SpectralCorrection(np.zeros(A.shape[0]), 32))
+    ref = np.zeros(A.shape[0])
+    for k in range(5):
+        ref = ref + [0.3, 0.5][k % 2] * (f - A.dot(ref))
+    assert np.array_equal(u, ref)      # smoothing is bitwise; correction adds exact zeros
+
+
+def test_full_size_fns_alternation():
+    """cfg4 size (1023^2): one hybrid step vs the oracle."""
+    rng = np.random.default_rng(4)
+    A = O.assemble_anisotropic(1e-3, rng.uniform(0, np.pi), 1024)
+    f = rng.standard_normal(A.shape[0])
+    lam = 0.01 * rng.standard_normal(A.shape[0])
+    w = np.full(8, 0.5)
+    u = GF.fns_lite_step(A, f, np.zeros(A.shape[0]), G.WeightSchedule(omega=w), 8,
+                         GF.SpectralCorrection(lam, 1024))
+    uo = O.fns_lite_step(A, f, np.zeros(A.shape[0]), w, 8, lam)
+    assert _rel(u, uo) <= RTOL
+
+
+def test_nonfinite_raises():
+    A = O.assemble_anisotropic(0.5, 0.3, 16)
+    f = np.ones(A.shape[0])
+    with pytest.raises(G.DivergenceError) as e:
+        GF.solve_fns(A, f, G.WeightSchedule(omega=[1e308, 1e308]), GF.SpectralCorrection(
+            np.zeros(A.shape[0]), 16), 4, max_iters=3)
+    assert e.value.inner_iteration == 4
