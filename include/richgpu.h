@@ -69,10 +69,13 @@ typedef struct rg_solver rg_solver;
 typedef struct rg_op_desc {
     int dtype;
     int kind;
-    int batch;
+    int batch;         /* systems (vectors) the operator is applied to */
     int side;
     const void* stencil;
     const void* diag;
+    int shared;        /* 1: the arrays hold ONE system's coefficients, applied
+                          to all `batch` systems (e.g. 4 right-hand sides of
+                          one Helmholtz problem); 0: one set per system */
 } rg_op_desc;
 
 /* Weight schedule for all systems of a batch (schedules.py:11-54).
@@ -155,6 +158,21 @@ int rg_dst2(const rg_dst* plan, const double* in, double* out, void* stream);
  * fns.py:43-44,80); lam is [batch][side*side] float64. */
 int rg_fns_correct(const rg_op* A, const rg_dst* plan, const double* lam, double* u,
                    const double* f, void* stream);
+
+/* ---- V-cycle pieces (multigrid.py:24-59,151-163) ---------------------------
+ * n = cells per side of the FINE grid (even); fine vectors have (n-1)^2
+ * entries, coarse ones (n/2-1)^2.  Bitwise equal to the reference's CSR
+ * R.matvec / P.matvec (power-of-two weights, CSR summation order). */
+int rg_restrict(int dtype, int batch, int n, const void* fine, void* coarse,
+                void* stream);
+/* fine += P coarse  (u = u + P.matvec(ec), multigrid.py:162) */
+int rg_prolong_add(int dtype, int batch, int n, const void* coarse, void* fine,
+                   void* stream);
+/* y[b] = M x[b] with M dense [n][n] row-major (one per system, or one shared
+ * when shared != 0): the coarsest-level solve with a precomputed inverse
+ * (replaces scipy.linalg.lu_solve, multigrid.py:155; ~1e-15 relative). */
+int rg_dense_apply(int dtype, int batch, int n, const void* M, int shared,
+                   const void* x, void* y, void* stream);
 
 /* ---- solve_stationary engine (richardson.py:77-141) ----------------------
  * A solver owns device workspace (per-system status, trace, reduction

@@ -26,7 +26,7 @@ VARIANT_CODE = {"plain": RG_PLAIN, "mom": RG_MOM, "nag": RG_NAG, "nagex": RG_NAG
 
 class rg_op_desc(C.Structure):
     _fields_ = [("dtype", C.c_int), ("kind", C.c_int), ("batch", C.c_int), ("side", C.c_int),
-                ("stencil", C.c_void_p), ("diag", C.c_void_p)]
+                ("stencil", C.c_void_p), ("diag", C.c_void_p), ("shared", C.c_int)]
 
 
 class rg_sched(C.Structure):
@@ -57,6 +57,9 @@ _SIGS = [
     ("rg_dst_destroy", _I, [_P]),
     ("rg_dst2", _I, [_P, _P, _P, _P]),
     ("rg_fns_correct", _I, [_P, _P, _P, _P, _P, _P]),
+    ("rg_restrict", _I, [_I, _I, _I, _P, _P, _P]),
+    ("rg_prolong_add", _I, [_I, _I, _I, _P, _P, _P]),
+    ("rg_dense_apply", _I, [_I, _I, _I, _P, _I, _P, _P, _P]),
     ("rg_solver_create", _I, [C.POINTER(_P), _P, C.POINTER(rg_sched), C.c_double, _I, _I, _I]),
     ("rg_solver_destroy", _I, [_P]),
     ("rg_solver_begin", _I, [_P, _P, _P, _P, _P, _P, _P]),

@@ -14,6 +14,7 @@
 #include "../../include/richgpu.h"
 #include "block.cuh"
 #include "dst.cuh"
+#include "mg.cuh"
 
 using namespace rg;
 
@@ -94,6 +95,7 @@ static OpView<S> view(const rg_op* A) {
     v.diag = (const S*)A->d.diag;
     v.side = A->d.side;
     v.P = A->P;
+    v.shared = A->d.shared;
     return v;
 }
 
@@ -333,7 +335,7 @@ int rg_op_create(rg_op** out, const rg_op_desc* d) {
     A->P = d->side * d->side;
     if (d->kind == RG_CONST9 && (d->dtype == RG_F64 || d->dtype == RG_F32)) {
         // the blocked sweep takes the 9 coefficients as kernel parameters
-        const size_t n = (size_t)d->batch * 9;
+        const size_t n = (size_t)(d->shared ? 1 : d->batch) * 9;
         A->hcoef.resize(n);
         cudaError_t e;
         if (d->dtype == RG_F64) {
@@ -346,6 +348,11 @@ int rg_op_create(rg_op** out, const rg_op_desc* d) {
         if (e != cudaSuccess) {
             delete A;
             return fail(RG_ECUDA, "reading CONST9 coefficients: %s", cudaGetErrorString(e));
+        }
+        if (d->shared) {   // replicate for the per-system parameter table
+            A->hcoef.resize((size_t)d->batch * 9);
+            for (int b = 1; b < d->batch; ++b)
+                for (int q = 0; q < 9; ++q) A->hcoef[(size_t)b * 9 + q] = A->hcoef[q];
         }
     }
     *out = A;
@@ -575,6 +582,50 @@ int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u
     if ((rc = dst_pass(D, 0, DST_PLAIN, D->work, D->work, nullptr, st))) return rc;
     if ((rc = dst_pass(D, 1, DST_TWICE_LAM, D->work, D->work, lam, st))) return rc;
     return dst_pass(D, 0, DST_ADD, D->work, u, nullptr, st);
+}
+
+static int mg_dtype_ok(int dtype) { return dtype == RG_F64 || dtype == RG_C128 || dtype == RG_F32; }
+
+int rg_restrict(int dtype, int batch, int n, const void* fine, void* coarse, void* stream) {
+    if (!fine || !coarse) return fail(RG_ENULL, "null vector");
+    if (!mg_dtype_ok(dtype)) return fail(RG_EINVAL, "bad dtype %d", dtype);
+    if (n < 4 || (n & 1) || batch < 1) return fail(RG_ESIZE, "grid side %d must be even and >= 4", n);
+    const int nf = n - 1, nc = n / 2 - 1;
+    const dim3 g((nc + MG_BX - 1) / MG_BX, (nc + MG_BY - 1) / MG_BY, batch), blk(MG_BX, MG_BY);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == RG_F64) restrict_kernel<double><<<g, blk, 0, st>>>((const double*)fine, (double*)coarse, nf, nc);
+    else if (dtype == RG_F32) restrict_kernel<float><<<g, blk, 0, st>>>((const float*)fine, (float*)coarse, nf, nc);
+    else restrict_kernel<double2><<<g, blk, 0, st>>>((const double2*)fine, (double2*)coarse, nf, nc);
+    LAUNCH_CHECK();
+    return RG_OK;
+}
+
+int rg_prolong_add(int dtype, int batch, int n, const void* coarse, void* fine, void* stream) {
+    if (!fine || !coarse) return fail(RG_ENULL, "null vector");
+    if (!mg_dtype_ok(dtype)) return fail(RG_EINVAL, "bad dtype %d", dtype);
+    if (n < 4 || (n & 1) || batch < 1) return fail(RG_ESIZE, "grid side %d must be even and >= 4", n);
+    const int nf = n - 1, nc = n / 2 - 1;
+    const dim3 g((nf + MG_BX - 1) / MG_BX, (nf + MG_BY - 1) / MG_BY, batch), blk(MG_BX, MG_BY);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == RG_F64) prolong_add_kernel<double><<<g, blk, 0, st>>>((const double*)coarse, (double*)fine, nf, nc);
+    else if (dtype == RG_F32) prolong_add_kernel<float><<<g, blk, 0, st>>>((const float*)coarse, (float*)fine, nf, nc);
+    else prolong_add_kernel<double2><<<g, blk, 0, st>>>((const double2*)coarse, (double2*)fine, nf, nc);
+    LAUNCH_CHECK();
+    return RG_OK;
+}
+
+int rg_dense_apply(int dtype, int batch, int n, const void* M, int shared, const void* x, void* y,
+                   void* stream) {
+    if (!M || !x || !y) return fail(RG_ENULL, "null argument");
+    if (!mg_dtype_ok(dtype)) return fail(RG_EINVAL, "bad dtype %d", dtype);
+    if (n < 1 || batch < 1) return fail(RG_ESIZE, "bad size");
+    const dim3 g((n + 7) / 8, batch);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == RG_F64) dense_apply_kernel<double><<<g, 256, 0, st>>>((const double*)M, shared, (const double*)x, (double*)y, n);
+    else if (dtype == RG_F32) dense_apply_kernel<float><<<g, 256, 0, st>>>((const float*)M, shared, (const float*)x, (float*)y, n);
+    else dense_apply_kernel<double2><<<g, 256, 0, st>>>((const double2*)M, shared, (const double2*)x, (double2*)y, n);
+    LAUNCH_CHECK();
+    return RG_OK;
 }
 
 int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double tol,

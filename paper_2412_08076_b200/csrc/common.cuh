@@ -62,6 +62,11 @@ __device__ __forceinline__ double sqacc(double acc, double x) { return fma(x, x,
 __device__ __forceinline__ double sqacc(double acc, double2 x) {
     return fma(x.y, x.y, fma(x.x, x.x, acc));
 }
+__device__ __forceinline__ float shfl_down(float v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ double shfl_down(double v, int o) { return __shfl_down_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ double2 shfl_down(double2 v, int o) {
+    return make_double2(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
+}
 __device__ __forceinline__ bool finite(float x)   { return isfinite(x); }
 __device__ __forceinline__ bool finite(double x)  { return isfinite(x); }
 __device__ __forceinline__ bool finite(double2 x) { return isfinite(x.x) && isfinite(x.y); }

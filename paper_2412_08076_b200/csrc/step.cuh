@@ -18,6 +18,7 @@ struct OpView {
     const S* diag;     // DIAG5 [B][P]
     int side;
     int P;
+    int shared;        // one coefficient set applied to every system of the batch
 };
 
 // y = A x at interior point (i, j) of system b, CSR column order, no FMA.
@@ -25,7 +26,8 @@ struct OpView {
 // Zero-padded terms add +-0 to an accumulator that is never -0, which is an
 // exact no-op, so boundary rows (fewer CSR entries) are reproduced bitwise.
 template <typename S, int KIND, class F>
-__device__ __forceinline__ S apply_op(const OpView<S>& A, int b, size_t idx, F X) {
+__device__ __forceinline__ S apply_op(const OpView<S>& A, int bv, size_t idx, F X) {
+    const int b = A.shared ? 0 : bv;   // coefficient set of vector system bv
     if (KIND == K_CONST9) {
         const S* c = A.stencil + (size_t)b * 9;
         S s = mul(c[0], X(-1, -1));

@@ -1,0 +1,222 @@
+"""GPU drop-in for the V-cycle (multigrid.py:71-163).
+
+    build_hierarchy(A, n, coarsest=8, schedules=None, batch=1) -> GpuHierarchy
+    GpuHierarchy.from_reference(h, batch=1)    (a richlab Hierarchy)
+    v_cycle(h, f, u=None, pre=1, post=1)       -> u like f
+
+Host setup (Galerkin R A P products, coarsest LU) is one-time host work,
+as in the reference (out of the hot path); it uses SciPy
+exactly like multigrid.py so the coarse operators are the reference's bit
+for bit.  Per cycle everything runs on the device:
+
+  smoother      rg_sweep, NAG/plain with fresh v and no preconditioner
+                (multigrid.py:126-138); 5-point Helmholtz fine level, 9-point
+                variable-coefficient Galerkin levels
+  residual      rg_residual (CSR-order stencil)
+  transfers     rg_restrict / rg_prolong_add (bitwise = R.matvec / P.matvec)
+  coarsest      rg_dense_apply with the precomputed inverse of the coarsest
+                operator (replaces lu_solve; ~1e-15 relative)
+
+A hierarchy serves `batch` right-hand sides of the same operator at once
+(the coefficient planes are shared, not replicated).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+import torch
+
+from . import _lib as L
+from .errors import DivergenceError
+from .operator import GpuStencilOperator, default_device, extract_planes, classify
+from .richardson import DeviceSchedule, _is_host
+
+
+class CoarseSolveError(RuntimeError):
+    """multigrid.py:20-21."""
+
+
+def _fw1d(n):
+    nc = n // 2
+    r = np.repeat(np.arange(nc - 1), 3)
+    c = (2 * np.arange(nc - 1)[:, None] + np.arange(3)[None, :]).reshape(-1)
+    return sp.csr_matrix((np.tile([0.25, 0.5, 0.25], nc - 1), (r, c)), shape=(nc - 1, n - 1))
+
+
+def _canonical(M):
+    M = sp.csr_matrix(M)
+    M.sum_duplicates()
+    M.sort_indices()
+    M.eliminate_zeros()
+    return M
+
+
+def restriction_matrix(n):
+    """multigrid.py:39-42 (host, for setup and checks)."""
+    r1 = _fw1d(n)
+    return _canonical(sp.kron(r1, r1, format="csr"))
+
+
+def prolongation_matrix(n):
+    """multigrid.py:45-49."""
+    p1 = (2.0 * _fw1d(n).T).tocsr()
+    return _canonical(sp.kron(p1, p1, format="csr"))
+
+
+def _csr(A):
+    if hasattr(A, "to_scipy"):
+        return _canonical(A.to_scipy())
+    return _canonical(A)
+
+
+class GpuLevel:
+    def __init__(self, n, op, sched):
+        self.n, self.op, self.sched = n, op, sched
+
+
+class GpuHierarchy:
+    """Device hierarchy for `batch` right-hand sides (multigrid.py:80-87)."""
+
+    def __init__(self, levels_csr, ns, coarsest_lu, schedules, batch=1, device=None):
+        self.device = torch.device(device) if device is not None else default_device()
+        self.batch = int(batch)
+        if schedules is not None and not isinstance(schedules, (list, tuple)):
+            schedules = [schedules] * (len(levels_csr) - 1)
+        self.levels = []
+        for k, (Ak, nk) in enumerate(zip(levels_csr, ns)):
+            s, planes, present = extract_planes(Ak)
+            kind, data = classify(s, planes, present)
+            dt = planes.dtype if np.iscomplexobj(planes) else np.dtype(np.float64)
+            if kind == "const9":
+                op = GpuStencilOperator("const9", s, data[None], None, dt, self.device, batch=batch)
+            elif kind == "diag5":
+                off, dg = data
+                op = GpuStencilOperator("diag5", s, off[None], dg[None], dt, self.device, batch=batch)
+            else:
+                op = GpuStencilOperator("var9", s, planes[None], None, dt, self.device, batch=batch)
+            sched = None
+            if schedules is not None and k < len(levels_csr) - 1 and k < len(schedules) \
+                    and schedules[k] is not None:
+                sched = DeviceSchedule(op, schedules[k], None)
+            self.levels.append(GpuLevel(nk, op, sched))
+        self.dtype = self.levels[0].op.np_dtype
+        self.tdtype = self.levels[0].op.torch_dtype
+        nc = self.levels[-1].op.P
+        inv = scipy.linalg.lu_solve(coarsest_lu, np.eye(nc, dtype=self.dtype))
+        if not np.all(np.isfinite(inv)):
+            raise CoarseSolveError("coarsest solve failed: non-finite inverse")
+        self.coarse_inv = torch.as_tensor(np.ascontiguousarray(inv)).to(self.device)
+        self.lib = L.load()
+        self._ws = {}
+
+    @property
+    def depth(self):
+        return len(self.levels)
+
+    @classmethod
+    def from_reference(cls, h, batch=1, device=None):
+        """Device copy of a richlab Hierarchy (levels' A, n, schedule; coarsest_lu)."""
+        return cls([lvl.A for lvl in h.levels], [lvl.n for lvl in h.levels], h.coarsest_lu,
+                   [lvl.schedule for lvl in h.levels[:-1]], batch=batch, device=device)
+
+    # ---- device V-cycle ---------------------------------------------------
+    def _buf(self, key, k):
+        t = self._ws.get((key, k))
+        if t is None:
+            t = torch.empty((self.batch, self.levels[k].op.P), dtype=self.tdtype,
+                            device=self.device)
+            self._ws[(key, k)] = t
+        return t
+
+    def _smooth(self, k, f, u, count):
+        """multigrid.py:126-138 on the device; returns the tensor holding u."""
+        lvl = self.levels[k]
+        if count == 0 or lvl.sched is None:
+            return u
+        m = lvl.sched.m
+        v0, v1 = self._buf("v0", k), self._buf("v1", k)
+        v0.zero_()
+        other = self._buf("ua", k) if u.data_ptr() != self._buf("ua", k).data_ptr() else self._buf("ub", k)
+        outb = C.c_int()
+        L.check(self.lib.rg_sweep(lvl.op.handle, C.byref(lvl.sched.struct), 0, count * m, 0,
+                                  L.ptr(u), L.ptr(other), L.ptr(v0), L.ptr(v1), L.ptr(f),
+                                  C.byref(outb), L.stream_ptr()))
+        return u if outb.value == 0 else other
+
+    def _level(self, k, f, u, pre, post):
+        lib, s = self.lib, L.stream_ptr()
+        if k == self.depth - 1:
+            y = self._buf("y", k)
+            L.check(lib.rg_dense_apply(self.levels[k].op.rg_dtype, self.batch, self.levels[k].op.P,
+                                       L.ptr(self.coarse_inv), 1, L.ptr(f), L.ptr(y), s))
+            return y
+        lvl = self.levels[k]
+        u = self._smooth(k, f, u, pre)
+        r = self._buf("r", k)
+        L.check(lib.rg_residual(lvl.op.handle, L.ptr(u), L.ptr(f), L.ptr(r), None, s))
+        fc = self._buf("f", k + 1)
+        L.check(lib.rg_restrict(lvl.op.rg_dtype, self.batch, lvl.n, L.ptr(r), L.ptr(fc), s))
+        uc = self._buf("ua", k + 1)
+        uc.zero_()
+        ec = self._level(k + 1, fc, uc, pre, post)
+        L.check(lib.rg_prolong_add(lvl.op.rg_dtype, self.batch, lvl.n, L.ptr(ec), L.ptr(u), s))
+        return self._smooth(k, f, u, post)
+
+    def apply(self, f, u=None, pre=1, post=1):
+        """One V-cycle on device tensors f, u [batch, P0]; returns a new tensor."""
+        op0 = self.levels[0].op
+        fd = self._buf("f", 0)
+        fd.copy_(f.reshape(fd.shape))
+        ud = self._buf("ua", 0)
+        if u is None:
+            ud.zero_()
+        else:
+            ud.copy_(u.reshape(ud.shape))
+        out = self._level(0, fd, ud, pre, post)
+        res = out.clone()
+        if not bool(torch.isfinite(res).all()):
+            m = self.levels[0].sched.m if self.levels[0].sched is not None else 0
+            raise DivergenceError("smoother produced a non-finite iterate",
+                                  inner_iteration=pre * m)
+        return res
+
+
+def build_hierarchy(A, n, coarsest=8, schedules=None, batch=1, device=None):
+    """multigrid.py:90-123: Galerkin-coarsen by 2 down to `coarsest` on the
+    host (SciPy, as the reference), then move every level to the device."""
+    if n < 2 * coarsest:
+        raise ValueError(f"n={n} leaves no room to coarsen to {coarsest}")
+    levels, ns, side, Al = [], [], n, _csr(A)
+    while side > coarsest:
+        R, P = restriction_matrix(side), prolongation_matrix(side)
+        levels.append(Al)
+        ns.append(side)
+        Al = _canonical((R @ Al @ P).tocsr())
+        side //= 2
+    levels.append(Al)
+    ns.append(side)
+    if (side - 1) ** 2 > 1024:
+        raise ValueError("coarsest level exceeds the direct-solve budget")
+    try:
+        lu = scipy.linalg.lu_factor(Al.toarray())
+    except (ValueError, scipy.linalg.LinAlgError) as exc:
+        raise CoarseSolveError(f"coarsest factorization failed: {exc}")
+    if not np.all(np.isfinite(lu[0])):
+        raise CoarseSolveError("coarsest factorization produced non-finite factors "
+                               "(singular coarse operator)")
+    return GpuHierarchy(levels, ns, lu, schedules, batch=batch, device=device)
+
+
+def v_cycle(h: GpuHierarchy, f, u=None, pre=1, post=1):
+    """multigrid.py:141-148: one V-cycle; numpy in -> numpy out."""
+    host = _is_host(f)
+    ft = torch.as_tensor(np.asarray(f) if host else f).to(h.device, h.tdtype)
+    ut = None if u is None else torch.as_tensor(np.asarray(u) if _is_host(u) else u).to(
+        h.device, h.tdtype)
+    out = h.apply(ft, ut, pre, post)
+    shp = np.shape(f) if host else f.shape
+    out = out.reshape(shp)
+    return out.cpu().numpy() if host else out

@@ -157,7 +157,10 @@ def as_numpy_dtype(dt):
 class GpuStencilOperator:
     """A batch of B structured-grid operators resident on the GPU."""
 
-    def __init__(self, kind, side, stencil, diag=None, dtype=np.float64, device=None):
+    def __init__(self, kind, side, stencil, diag=None, dtype=np.float64, device=None, batch=None):
+        """stencil/diag hold one coefficient set per system ([B, ...]); with
+        `batch` > len(stencil) == 1 the single set is shared by `batch`
+        systems (several right-hand sides of one operator)."""
         self.device = torch.device(device) if device is not None else default_device()
         self.np_dtype = as_numpy_dtype(dtype)
         if self.np_dtype not in _DTYPES:
@@ -167,7 +170,11 @@ class GpuStencilOperator:
         self.side = int(side)
         self.P = self.side * self.side
         st = np.asarray(stencil)
-        self.batch = st.shape[0]
+        self.nsets = st.shape[0]
+        self.batch = int(batch) if batch is not None else self.nsets
+        self.shared = self.nsets == 1 and self.batch > 1
+        if self.nsets != self.batch and not self.shared:
+            raise DimensionMismatch(f"{self.nsets} coefficient sets for {self.batch} systems")
         self._host_stencil = st.astype(self.np_dtype)
         self._host_diag = None if diag is None else np.asarray(diag).astype(self.np_dtype)
         self.stencil = torch.as_tensor(np.ascontiguousarray(self._host_stencil)).to(self.device)
@@ -176,7 +183,8 @@ class GpuStencilOperator:
         lib = L.load()
         d = L.rg_op_desc(self.rg_dtype, self.kind, self.batch, self.side,
                          self.stencil.data_ptr(),
-                         self.diag.data_ptr() if self.diag is not None else None)
+                         self.diag.data_ptr() if self.diag is not None else None,
+                         1 if self.shared else 0)
         h = C.c_void_p()
         L.check(lib.rg_op_create(C.byref(h), C.byref(d)))
         self._h = h
@@ -256,6 +264,7 @@ class GpuStencilOperator:
 
     def diagonal(self, b=0):
         """Main diagonal of system b as a host array (sparse.py:116-117)."""
+        b = 0 if self.shared else b
         if self.kind == L.RG_CONST9:
             c = self._host_stencil[b, 4]
             return np.full(self.P, c, dtype=self.np_dtype)
@@ -286,7 +295,7 @@ class GpuStencilOperator:
     def transpose(self):
         if self.kind == L.RG_CONST9:
             return GpuStencilOperator("const9", self.side, self._host_stencil[:, ::-1].copy(),
-                                      None, self.np_dtype, self.device)
+                                      None, self.np_dtype, self.device, batch=self.batch)
         planes = self._full_planes()
         s = self.side
         t = np.zeros_like(planes)
@@ -297,14 +306,14 @@ class GpuStencilOperator:
             src = np.nonzero(ok)[0]
             nb = (x[src] + dx) * s + (y[src] + dy)
             t[:, q, src] = planes[:, 8 - q, nb]
-        return GpuStencilOperator("var9", s, t, None, self.np_dtype, self.device)
+        return GpuStencilOperator("var9", s, t, None, self.np_dtype, self.device, batch=self.batch)
 
     def _full_planes(self):
         if self.kind == L.RG_VAR9:
             return self._host_stencil
-        planes = np.zeros((self.batch, 9, self.P), dtype=self.np_dtype)
+        planes = np.zeros((self.nsets, 9, self.P), dtype=self.np_dtype)
         inside = _neighbour_mask(self.side)
-        for b in range(self.batch):
+        for b in range(self.nsets):
             if self.kind == L.RG_CONST9:
                 planes[b] = np.where(inside, self._host_stencil[b][:, None], 0)
             else:
@@ -323,7 +332,7 @@ class GpuStencilOperator:
         return r, n2
 
     def __repr__(self):
-        return (f"GpuStencilOperator({_KIND_NAMES[self.kind]}, batch={self.batch}, "
+        return (f"GpuStencilOperator({_KIND_NAMES[self.kind]}, batch={self.batch}, shared={self.shared}, "
                 f"side={self.side}, dtype={self.np_dtype})")
 
 
