@@ -241,6 +241,13 @@ class GpuStencilOperator:
         dg = None if ops[0]._host_diag is None else np.concatenate([o._host_diag for o in ops])
         return cls(_KIND_NAMES[k], s, st, dg, dt, ops[0].device)
 
+    def broadcast(self, batch):
+        """The same operator applied to `batch` systems (shared coefficients)."""
+        if self.nsets != 1:
+            raise DimensionMismatch("only a single-system operator can be broadcast")
+        return GpuStencilOperator(_KIND_NAMES[self.kind], self.side, self._host_stencil,
+                                  self._host_diag, self.np_dtype, self.device, batch=batch)
+
     # ---- reference duck-typing -------------------------------------------
     @property
     def nrows(self):
