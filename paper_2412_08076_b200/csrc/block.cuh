@@ -40,8 +40,8 @@ constexpr int BLK_MAXB = 64;   // systems per launch (coefficients ride in the p
 
 template <typename S>
 struct BlockArgs {
-    S coef[BLK_MAXB][9];   // CSR-order stencil of systems b0 .. b0+gridDim.y-1
-    S scale[BLK_MAXB];     // Jacobi scale (JAC instantiations)
+    CT<S> coef[BLK_MAXB][9];   // CSR-order stencil of systems b0 .. b0+gridDim.y-1
+    CT<S> scale[BLK_MAXB];     // Jacobi scale (JAC instantiations)
     int b0;                // first system of this launch
     int side;
     int P;
@@ -65,10 +65,10 @@ struct BlockArgs {
 #ifndef RG_MINB_PLAIN_F64
 #define RG_MINB_PLAIN_F64 2
 #endif
+// (f32 storage computes in f64, so the register budget does not depend on S)
 template <typename S, int VAR>
 struct BlockMinCtas {
-    static constexpr int value = (VAR == V_PLAIN) ? (sizeof(S) == 8 ? RG_MINB_PLAIN_F64 : 3)
-                                                  : (VAR == V_MOM ? 2 : (sizeof(S) == 8 ? 1 : 2));
+    static constexpr int value = (VAR == V_PLAIN) ? RG_MINB_PLAIN_F64 : (VAR == V_MOM ? 2 : 1);
 };
 
 // Tile shape used by the library (load window LR x LC, NW warps).
@@ -96,8 +96,9 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
     static_assert(LR % NW == 0 && LC % 32 == 0 && T >= 1 && TX > 0 && TY > 0, "tile");
     static_assert(RPW * CPT <= 32, "domain mask");
 
+    typedef CT<S> C;   // arithmetic type (f32 storage computes in f64)
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    typedef S Row[LC];
+    typedef C Row[LC];
     Row* buf0 = reinterpret_cast<Row*>(smem_raw);
     Row* buf1 = buf0 + LR;
 
@@ -113,12 +114,12 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
     const size_t base = (size_t)b * a.P;
     const int r0 = wp * RPW;
 
-    S c[9];
+    C c[9];
 #pragma unroll
     for (int d = 0; d < 9; ++d) c[d] = a.coef[bl][d];
-    const S sc = JAC ? a.scale[bl] : szero<S>();
+    const C sc = JAC ? a.scale[bl] : szero<C>();
 
-    S fr[RPW][CPT], vr[RPW][CPT], ur[RPW][CPT];
+    C fr[RPW][CPT], vr[RPW][CPT], ur[RPW][CPT];
     uint32_t dom = 0;  // bit (rr*CPT+cc): point inside the interior grid
 
     const double at0 = NAG ? a.atil[b * a.m + (a.k0 % a.m)] : 0.0;
@@ -131,12 +132,12 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
             const int gy = gy0 + col;
             const bool in = (gx >= 0) && (gx < side) && (gy >= 0) && (gy < side);
             const size_t g = base + (size_t)gx * side + gy;
-            const S u = in ? a.u_in[g] : szero<S>();
-            fr[rr][cc] = in ? a.f[g] : szero<S>();
-            vr[rr][cc] = (HASV && in) ? a.v_in[g] : szero<S>();
+            const C u = in ? to_c(a.u_in[g]) : szero<C>();
+            fr[rr][cc] = in ? to_c(a.f[g]) : szero<C>();
+            vr[rr][cc] = (HASV && in) ? to_c(a.v_in[g]) : szero<C>();
             if (NAG) ur[rr][cc] = u;
             if (in) dom |= 1u << (rr * CPT + cc);
-            S x = u;
+            C x = u;
             if (NAG && in) x = add(x, rmul(at0, vr[rr][cc]));  // y = u + at*v
             buf0[r0 + rr][col] = x;
             if (NAG && a.norm_first_u) buf1[r0 + rr][col] = u;
@@ -160,7 +161,7 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
             cp[cc] = cl[cc] < LC - 1 ? cl[cc] + 1 : LC - 1;
         }
         const int rm = r0 > 0 ? r0 - 1 : 0;
-        S w0[CPT], w1[CPT], w2[CPT], x0[CPT], x1[CPT], x2[CPT];
+        C w0[CPT], w1[CPT], w2[CPT], x0[CPT], x1[CPT], x2[CPT];
 #pragma unroll
         for (int cc = 0; cc < CPT; ++cc) {
             w0[cc] = src[rm][cm[cc]]; w1[cc] = src[rm][cl[cc]]; w2[cc] = src[rm][cp[cc]];
@@ -170,7 +171,7 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
         for (int rr = 0; rr < RPW; ++rr) {
             const int r = r0 + rr;
             const int rp = r + 1 < LR ? r + 1 : LR - 1;
-            S y0[CPT], y1[CPT], y2[CPT], s[CPT];
+            C y0[CPT], y1[CPT], y2[CPT], s[CPT];
 #pragma unroll
             for (int cc = 0; cc < CPT; ++cc) {
                 y0[cc] = src[rp][cm[cc]]; y1[cc] = src[rp][cl[cc]]; y2[cc] = src[rp][cp[cc]];
@@ -208,8 +209,8 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
 
     if (NAG && a.norm_first_u) {
         // residual at u itself for the sweep-boundary convergence test (:124-125)
-        sweep_rows(buf1, [&](int rr, int cc, int r, int col, S s, S) {
-            const S rs = (owned(r, col) && indom(rr, cc)) ? sub(fr[rr][cc], s) : szero<S>();
+        sweep_rows(buf1, [&](int rr, int cc, int r, int col, C s, C) {
+            const C rs = (owned(r, col) && indom(rr, cc)) ? sub(fr[rr][cc], s) : szero<C>();
             acc[0] = sqacc(acc[0], rs);
         });
         __syncthreads();
@@ -229,28 +230,29 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
             Row* cur = (t & 1) ? buf1 : buf0;
             Row* nxt = (t & 1) ? buf0 : buf1;
             const bool last = (t == T - 1);
-            sweep_rows(cur, [&](int rr, int cc, int r, int col, S s, S centre) {
+            sweep_rows(cur, [&](int rr, int cc, int r, int col, C s, C centre) {
                 const bool live = INTERIOR || indom(rr, cc);
-                const S rs = sub(fr[rr][cc], s);                        // r = f - A x
+                const C rs = sub(fr[rr][cc], s);                        // r = f - A x
                 if (!NAG && a.norm_every) {
-                    const S rn = (live && owned(r, col)) ? rs : szero<S>();
+                    const C rn = (live && owned(r, col)) ? rs : szero<C>();
                     acc[(NACC > 1) ? t : 0] = sqacc(acc[(NACC > 1) ? t : 0], rn);
                 }
-                const S p = JAC ? mul(sc, rs) : rs;                      // B^{-1} r
-                S vn;
+                const C p = JAC ? mul(sc, rs) : rs;                      // B^{-1} r
+                C vn;
                 if (VAR == V_PLAIN) vn = rmul(w, p);
                 else vn = add(rmul(al, vr[rr][cc]), rmul(w, p));         // v = a v + w p
-                const S uo = NAG ? ur[rr][cc] : centre;                  // plain/mom: x == u
-                const S un = add(uo, vn);                                // u = u + v
+                const C uo = NAG ? ur[rr][cc] : centre;                  // plain/mom: x == u
+                const C un = stored<S>(add(uo, vn));                     // u = u + v (as stored)
+                vn = stored<S>(vn);
                 if (HASV) vr[rr][cc] = vn;
                 if (NAG) ur[rr][cc] = un;
                 if (!last) {
-                    const S x = NAG ? add(un, rmul(atn, vn)) : un;       // next stencil input
-                    nxt[r][col] = live ? x : szero<S>();
+                    const C x = NAG ? add(un, rmul(atn, vn)) : un;       // next stencil input
+                    nxt[r][col] = live ? x : szero<C>();
                 } else if (live && owned(r, col)) {
                     const size_t g = base + (size_t)(gx0 + r) * side + (gy0 + col);
-                    a.u_out[g] = un;
-                    if (HASV) a.v_out[g] = vn;
+                    a.u_out[g] = to_s<S>(un);
+                    if (HASV) a.v_out[g] = to_s<S>(vn);
                 }
             });
             if (!last) __syncthreads();
@@ -269,7 +271,7 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
 template <typename S, int VAR, int T, bool JAC>
 cudaError_t launch_block_t(const BlockArgs<S>& a, int nsys, cudaStream_t st) {
     auto kern = block_kernel<S, VAR, T, BLK_LR, BLK_LC, BLK_NW, JAC>;
-    const size_t smem = 2 * (size_t)BLK_LR * BLK_LC * sizeof(S);
+    const size_t smem = 2 * (size_t)BLK_LR * BLK_LC * sizeof(CT<S>);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -91,8 +91,8 @@ static dim3 step_grid(const rg_op* A) {
 template <typename S>
 static OpView<S> view(const rg_op* A) {
     OpView<S> v;
-    v.stencil = (const S*)A->d.stencil;
-    v.diag = (const S*)A->d.diag;
+    v.stencil = (const CT<S>*)A->d.stencil;
+    v.diag = (const CT<S>*)A->d.diag;
     v.side = A->d.side;
     v.P = A->P;
     v.shared = A->d.shared;
@@ -142,7 +142,7 @@ static int do_step1(const rg_op* A, const StepReq& q, cudaStream_t st) {
     a.omega = q.omega;
     a.alpha = q.alpha;
     a.atil = q.atil;
-    a.scale = (const S*)q.scale;
+    a.scale = (const CT<S>*)q.scale;
     a.m = q.m;
     a.i = q.i;
     a.variant = q.variant;
@@ -204,8 +204,8 @@ static int do_block(rg_solver* S_, int T, int norm_first_u, cudaStream_t st) {
         const int nsys = B - b0 < BLK_MAXB ? B - b0 : BLK_MAXB;
         a.b0 = b0;
         for (int j = 0; j < nsys; ++j) {
-            for (int d = 0; d < 9; ++d) a.coef[j][d] = (S)A->hcoef[(size_t)(b0 + j) * 9 + d];
-            a.scale[j] = jac ? (S)S_->hscale[b0 + j] : (S)0;
+            for (int d = 0; d < 9; ++d) a.coef[j][d] = A->hcoef[(size_t)(b0 + j) * 9 + d];
+            a.scale[j] = jac ? S_->hscale[b0 + j] : 0.0;
         }
         cudaError_t err;
         switch (S_->s.variant) {
@@ -299,8 +299,8 @@ static int sweep_block(const rg_op* A, const rg_sched* s, int k0, int T, bool ja
         const int nsys = B - b0 < BLK_MAXB ? B - b0 : BLK_MAXB;
         a.b0 = b0;
         for (int j = 0; j < nsys; ++j) {
-            for (int d = 0; d < 9; ++d) a.coef[j][d] = (S)A->hcoef[(size_t)(b0 + j) * 9 + d];
-            a.scale[j] = jac_scalar ? (S)hscale[b0 + j] : (S)0;
+            for (int d = 0; d < 9; ++d) a.coef[j][d] = A->hcoef[(size_t)(b0 + j) * 9 + d];
+            a.scale[j] = jac_scalar ? hscale[b0 + j] : 0.0;
         }
         cudaError_t err;
         switch (s->variant) {
@@ -338,13 +338,8 @@ int rg_op_create(rg_op** out, const rg_op_desc* d) {
         const size_t n = (size_t)(d->shared ? 1 : d->batch) * 9;
         A->hcoef.resize(n);
         cudaError_t e;
-        if (d->dtype == RG_F64) {
-            e = cudaMemcpy(A->hcoef.data(), d->stencil, n * sizeof(double), cudaMemcpyDeviceToHost);
-        } else {
-            std::vector<float> tmp(n);
-            e = cudaMemcpy(tmp.data(), d->stencil, n * sizeof(float), cudaMemcpyDeviceToHost);
-            for (size_t i = 0; i < n; ++i) A->hcoef[i] = tmp[i];
-        }
+        // coefficients are float64 for both F64 and F32 operators
+        e = cudaMemcpy(A->hcoef.data(), d->stencil, n * sizeof(double), cudaMemcpyDeviceToHost);
         if (e != cudaSuccess) {
             delete A;
             return fail(RG_ECUDA, "reading CONST9 coefficients: %s", cudaGetErrorString(e));
@@ -469,15 +464,8 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     if (blocked && jac) {
         const int B = A->d.batch;
         hscale.resize(B);
-        if (A->d.dtype == RG_F64) {
-            CUDA_TRY(cudaMemcpyAsync(hscale.data(), s->scale, B * sizeof(double), cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-        } else {
-            std::vector<float> tmp(B);
-            CUDA_TRY(cudaMemcpyAsync(tmp.data(), s->scale, B * sizeof(float), cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            for (int b = 0; b < B; ++b) hscale[b] = tmp[b];
-        }
+        CUDA_TRY(cudaMemcpyAsync(hscale.data(), s->scale, B * sizeof(double), cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
     }
     const int T = block_T == 0 ? (s->variant >= RG_NAG ? 6 : 5) : block_T;
     int k = i0;
@@ -729,18 +717,10 @@ int rg_solver_begin(rg_solver* S, void* u0, void* u1, void* v0, void* v1, const 
     if (S->use_block && S->s.precond == RG_PRECOND_JACOBI_SCALAR) {
         // the blocked sweep takes the per-system Jacobi scale as a kernel parameter
         const int B = A->d.batch;
-        S->hscale.resize(B);
-        if (A->d.dtype == RG_F64) {
-            CUDA_TRY(cudaMemcpyAsync(S->hscale.data(), S->s.scale, B * sizeof(double),
-                                     cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-        } else {
-            std::vector<float> tmp(B);
-            CUDA_TRY(cudaMemcpyAsync(tmp.data(), S->s.scale, B * sizeof(float),
-                                     cudaMemcpyDeviceToHost, st));
-            CUDA_TRY(cudaStreamSynchronize(st));
-            for (int b = 0; b < B; ++b) S->hscale[b] = tmp[b];
-        }
+        S->hscale.resize(B);   // Jacobi scales are float64 for F64 and F32 operators
+        CUDA_TRY(cudaMemcpyAsync(S->hscale.data(), S->s.scale, B * sizeof(double),
+                                 cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
     }
     CUDA_TRY(cudaMemsetAsync(S->d_st, 0, sizeof(SysState) * A->d.batch, st));
     CUDA_TRY(cudaMemsetAsync(S->d_trace, 0, sizeof(double) * A->d.batch * (size_t)S->trace_stride, st));

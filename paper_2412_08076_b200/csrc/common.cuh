@@ -23,6 +23,24 @@ enum { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_DIVERGED = 2, ST_MAXED = 3 };
 template <typename S> struct Real { typedef S type; };
 template <> struct Real<double2> { typedef double type; };
 
+// Arithmetic type for a storage type: float32 vectors are computed in
+// float64 (loaded -> widened, rounded once on store), so the f32 mode keeps
+// f32 HBM traffic but the reference's float64 arithmetic; coefficients and
+// Jacobi scales of an f32 operator are float64.
+template <typename S> struct Compute { typedef S type; };
+template <> struct Compute<float> { typedef double type; };
+template <typename S> using CT = typename Compute<S>::type;
+
+__device__ __forceinline__ double  to_c(float x)   { return (double)x; }
+__device__ __forceinline__ double  to_c(double x)  { return x; }
+__device__ __forceinline__ double2 to_c(double2 x) { return x; }
+template <typename S> __device__ __forceinline__ S to_s(CT<S> x);
+template <> __device__ __forceinline__ float   to_s<float>(double x)    { return (float)x; }
+template <> __device__ __forceinline__ double  to_s<double>(double x)   { return x; }
+template <> __device__ __forceinline__ double2 to_s<double2>(double2 x) { return x; }
+// value as stored and reloaded: the rounding a state vector sees per step
+template <typename S> __device__ __forceinline__ CT<S> stored(CT<S> x) { return to_c(to_s<S>(x)); }
+
 __device__ __forceinline__ float   zero(float*)   { return 0.f; }
 __device__ __forceinline__ double  zero(double*)  { return 0.0; }
 __device__ __forceinline__ double2 zero(double2*) { return make_double2(0.0, 0.0); }

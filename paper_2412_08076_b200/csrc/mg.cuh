@@ -23,13 +23,13 @@ restrict_kernel(const S* __restrict__ fine, S* __restrict__ coarse, int nf, int 
     if (I >= nc || J >= nc) return;
     const S* x = fine + (size_t)b * nf * nf + (size_t)(2 * I) * nf + 2 * J;
     const double w[3] = {0.25, 0.5, 0.25};
-    S s = rmul(w[0] * w[0], x[0]);
+    CT<S> s = rmul(w[0] * w[0], to_c(x[0]));
 #pragma unroll
     for (int q = 1; q < 9; ++q) {
         const int a = q / 3, c = q % 3;
-        s = add(s, rmul(w[a] * w[c], x[(size_t)a * nf + c]));
+        s = add(s, rmul(w[a] * w[c], to_c(x[(size_t)a * nf + c])));
     }
-    coarse[(size_t)b * nc * nc + (size_t)I * nc + J] = s;
+    coarse[(size_t)b * nc * nc + (size_t)I * nc + J] = to_s<S>(s);
 }
 
 // fine[p, q] = fine[p, q] + sum_{I in I(p)} sum_{J in J(q)} (pw_I pw_J) e[I, J]
@@ -55,16 +55,16 @@ prolong_add_kernel(const S* __restrict__ e, S* __restrict__ fine, int nf, int nc
         if (q / 2 < nc) { Jj[nj] = q / 2; wj[nj++] = 0.5; }
     }
     const S* ec = e + (size_t)b * nc * nc;
-    S s = szero<S>();
+    CT<S> s = szero<CT<S>>();
     bool first = true;
     for (int i = 0; i < ni; ++i)
         for (int j = 0; j < nj; ++j) {
-            const S t = rmul(wi[i] * wj[j], ec[(size_t)Ii[i] * nc + Jj[j]]);
+            const CT<S> t = rmul(wi[i] * wj[j], to_c(ec[(size_t)Ii[i] * nc + Jj[j]]));
             s = first ? t : add(s, t);
             first = false;
         }
     S* u = fine + (size_t)b * nf * nf + (size_t)p * nf + q;
-    if (!first) *u = add(*u, s);   // u = u + P e  (multigrid.py:162)
+    if (!first) *u = to_s<S>(add(to_c(*u), s));   // u = u + P e  (multigrid.py:162)
 }
 
 // y[b] = M[bm] x[b], M dense [n][n] row-major (coarsest-level inverse), one
@@ -79,11 +79,11 @@ __global__ void __launch_bounds__(256) dense_apply_kernel(const S* __restrict__ 
     if (row >= n) return;
     const S* Mr = M + (shared ? 0 : (size_t)b * n * n) + (size_t)row * n;
     const S* xb = x + (size_t)b * n;
-    S s = szero<S>();
-    for (int j = lane; j < n; j += 32) s = add(s, mul(Mr[j], xb[j]));
+    CT<S> s = szero<CT<S>>();
+    for (int j = lane; j < n; j += 32) s = add(s, mul(to_c(Mr[j]), to_c(xb[j])));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s = add(s, shfl_down(s, o));
-    if (lane == 0) y[(size_t)b * n + row] = s;
+    if (lane == 0) y[(size_t)b * n + row] = to_s<S>(s);
 }
 
 }  // namespace rg

@@ -14,8 +14,8 @@ namespace rg {
 
 template <typename S>
 struct OpView {
-    const S* stencil;  // CONST9 [B][9] | DIAG5 [B][4] | VAR9 [B][9][P]
-    const S* diag;     // DIAG5 [B][P]
+    const CT<S>* stencil;  // CONST9 [B][9] | DIAG5 [B][4] | VAR9 [B][9][P] (arithmetic type)
+    const CT<S>* diag;     // DIAG5 [B][P]
     int side;
     int P;
     int shared;        // one coefficient set applied to every system of the batch
@@ -26,11 +26,12 @@ struct OpView {
 // Zero-padded terms add +-0 to an accumulator that is never -0, which is an
 // exact no-op, so boundary rows (fewer CSR entries) are reproduced bitwise.
 template <typename S, int KIND, class F>
-__device__ __forceinline__ S apply_op(const OpView<S>& A, int bv, size_t idx, F X) {
+__device__ __forceinline__ CT<S> apply_op(const OpView<S>& A, int bv, size_t idx, F X) {
+    typedef CT<S> C;
     const int b = A.shared ? 0 : bv;   // coefficient set of vector system bv
     if (KIND == K_CONST9) {
-        const S* c = A.stencil + (size_t)b * 9;
-        S s = mul(c[0], X(-1, -1));
+        const C* c = A.stencil + (size_t)b * 9;
+        C s = mul(c[0], X(-1, -1));
         s = add(s, mul(c[1], X(-1, 0)));
         s = add(s, mul(c[2], X(-1, 1)));
         s = add(s, mul(c[3], X(0, -1)));
@@ -41,17 +42,17 @@ __device__ __forceinline__ S apply_op(const OpView<S>& A, int bv, size_t idx, F 
         s = add(s, mul(c[8], X(1, 1)));
         return s;
     } else if (KIND == K_DIAG5) {
-        const S* c = A.stencil + (size_t)b * 4;
-        S s = mul(c[0], X(-1, 0));
+        const C* c = A.stencil + (size_t)b * 4;
+        C s = mul(c[0], X(-1, 0));
         s = add(s, mul(c[1], X(0, -1)));
         s = add(s, mul(A.diag[(size_t)b * A.P + idx], X(0, 0)));
         s = add(s, mul(c[2], X(0, 1)));
         s = add(s, mul(c[3], X(1, 0)));
         return s;
     } else {  // K_VAR9: planes [b][d][P]
-        const S* c = A.stencil + (size_t)b * 9 * A.P + idx;
+        const C* c = A.stencil + (size_t)b * 9 * A.P + idx;
         const size_t P = A.P;
-        S s = mul(c[0], X(-1, -1));
+        C s = mul(c[0], X(-1, -1));
         s = add(s, mul(c[1 * P], X(-1, 0)));
         s = add(s, mul(c[2 * P], X(-1, 1)));
         s = add(s, mul(c[3 * P], X(0, -1)));
@@ -76,7 +77,7 @@ struct StepArgs {
     const double* omega;
     const double* alpha;
     const double* atil;
-    const S* scale;    // Jacobi scale (P_JSCALAR: [B], P_JFIELD: [B][P])
+    const CT<S>* scale;  // Jacobi scale (P_JSCALAR: [B], P_JFIELD: [B][P])
     int m;
     int i;             // schedule index of this inner step
     int variant;       // V_*
@@ -108,59 +109,61 @@ __global__ void __launch_bounds__(STEP_NT) step1_kernel(StepArgs<S> a) {
     const bool nag = a.variant >= V_NAG;
     const int si = b * a.m + a.i;
 
+    typedef CT<S> C;
     double acc[1] = {0.0};
     double facc = 0.0;
     if (in) {
         const S* u = a.u_in + base;
         const S* v = a.v_in ? a.v_in + base : nullptr;
-        auto Xu = [&](int di, int dj) -> S {
+        auto Xu = [&](int di, int dj) -> C {
             const int ii = i + di, jj = j + dj;
-            if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<S>();
-            return u[idx + (ptrdiff_t)di * side + dj];
+            if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
+            return to_c(u[idx + (ptrdiff_t)di * side + dj]);
         };
-        const S fi = a.f ? a.f[base + idx] : szero<S>();
-        S r = szero<S>();
+        const C fi = a.f ? to_c(a.f[base + idx]) : szero<C>();
+        C r = szero<C>();
         if (!nag || !a.update) {
             // plain / mom: the step residual is the residual at u (:116-117)
-            const S s = apply_op<S, KIND>(a.A, b, idx, Xu);
+            const C s = apply_op<S, KIND>(a.A, b, idx, Xu);
             r = sub(fi, s);
             if (a.norm_u) acc[0] = sqacc(acc[0], r);
         } else {
             // nag / nagex: residual at the look-ahead u + at*v (:118-119)
             const double at = a.atil[si];
-            auto Xy = [&](int di, int dj) -> S {
+            auto Xy = [&](int di, int dj) -> C {
                 const int ii = i + di, jj = j + dj;
-                if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<S>();
+                if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
                 const size_t q = idx + (ptrdiff_t)di * side + dj;
-                S x = u[q];
-                if (v) x = add(x, rmul(at, v[q]));
+                C x = to_c(u[q]);
+                if (v) x = add(x, rmul(at, to_c(v[q])));
                 return x;
             };
-            const S s = apply_op<S, KIND>(a.A, b, idx, Xy);
+            const C s = apply_op<S, KIND>(a.A, b, idx, Xy);
             r = sub(fi, s);
             if (a.norm_u) {  // convergence residual at u itself (:124-125)
-                const S su = apply_op<S, KIND>(a.A, b, idx, Xu);
+                const C su = apply_op<S, KIND>(a.A, b, idx, Xu);
                 acc[0] = sqacc(acc[0], sub(fi, su));
             }
         }
-        if (a.r_out) a.r_out[base + idx] = r;
+        if (a.r_out) a.r_out[base + idx] = to_s<S>(r);
         if (a.update) {
-            S p = r;  // precond.py:125-129
+            C p = r;  // precond.py:125-129
             if (a.precond == P_JSCALAR) p = mul(a.scale[b], r);
             else if (a.precond == P_JFIELD) p = mul(a.scale[base + idx], r);
             const double w = a.omega[si];
-            const S ui = u[idx];
-            S vn;
+            const C ui = to_c(u[idx]);
+            C vn;
             if (a.variant == V_PLAIN) {
                 vn = rmul(w, p);  // 0*v + w*p == w*p for finite v
             } else {
-                const S vi = v ? v[idx] : szero<S>();
+                const C vi = v ? to_c(v[idx]) : szero<C>();
                 vn = add(rmul(a.alpha[si], vi), rmul(w, p));  // :120 / :58
             }
-            const S un = add(ui, vn);  // :121 / :59
-            a.u_out[base + idx] = un;
-            if (a.v_out) a.v_out[base + idx] = vn;
-            if (a.nonfinite_at && !(finite(un) && finite(vn))) atomicMin(&a.nonfinite_at[b], a.tag);
+            const S vs = to_s<S>(vn);
+            const S us = to_s<S>(add(ui, vn));  // :121 / :59 (u + v from the unrounded v)
+            a.u_out[base + idx] = us;
+            if (a.v_out) a.v_out[base + idx] = vs;
+            if (a.nonfinite_at && !(finite(us) && finite(vs))) atomicMin(&a.nonfinite_at[b], a.tag);
         }
         if (a.epi.with_f) facc = sqacc(facc, fi);
     }
@@ -174,6 +177,7 @@ __global__ void __launch_bounds__(STEP_NT) step1_kernel(StepArgs<S> a) {
 // y = A x (sparse.py:101-106), batched.
 template <typename S, int KIND>
 __global__ void __launch_bounds__(STEP_NT) matvec_kernel(OpView<S> A, const S* x, S* y) {
+    typedef CT<S> C;
     const int b = blockIdx.z;
     const int side = A.side;
     const int j = blockIdx.x * STEP_BX + threadIdx.x;
@@ -182,12 +186,12 @@ __global__ void __launch_bounds__(STEP_NT) matvec_kernel(OpView<S> A, const S* x
     const size_t base = (size_t)b * A.P;
     const size_t idx = (size_t)i * side + j;
     const S* xs = x + base;
-    auto X = [&](int di, int dj) -> S {
+    auto X = [&](int di, int dj) -> C {
         const int ii = i + di, jj = j + dj;
-        if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<S>();
-        return xs[idx + (ptrdiff_t)di * side + dj];
+        if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
+        return to_c(xs[idx + (ptrdiff_t)di * side + dj]);
     };
-    y[base + idx] = apply_op<S, KIND>(A, b, idx, X);
+    y[base + idx] = to_s<S>(apply_op<S, KIND>(A, b, idx, X));
 }
 
 }  // namespace rg

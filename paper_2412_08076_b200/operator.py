@@ -175,8 +175,13 @@ class GpuStencilOperator:
         self.shared = self.nsets == 1 and self.batch > 1
         if self.nsets != self.batch and not self.shared:
             raise DimensionMismatch(f"{self.nsets} coefficient sets for {self.batch} systems")
-        self._host_stencil = st.astype(self.np_dtype)
-        self._host_diag = None if diag is None else np.asarray(diag).astype(self.np_dtype)
+        # coefficients are float64 (complex128) even for float32 vectors: the
+        # f32 mode stores vectors in f32 but computes in f64 (csrc/common.cuh)
+        self.coef_np_dtype = np.dtype(np.complex128 if np.iscomplexobj(np.zeros(0, self.np_dtype))
+                                      else np.float64)
+        self.coef_torch_dtype = _DTYPES[self.coef_np_dtype][1]
+        self._host_stencil = st.astype(self.coef_np_dtype)
+        self._host_diag = None if diag is None else np.asarray(diag).astype(self.coef_np_dtype)
         self.stencil = torch.as_tensor(np.ascontiguousarray(self._host_stencil)).to(self.device)
         self.diag = None if diag is None else torch.as_tensor(
             np.ascontiguousarray(self._host_diag)).to(self.device)
@@ -274,7 +279,7 @@ class GpuStencilOperator:
         b = 0 if self.shared else b
         if self.kind == L.RG_CONST9:
             c = self._host_stencil[b, 4]
-            return np.full(self.P, c, dtype=self.np_dtype)
+            return np.full(self.P, c, dtype=self.coef_np_dtype)
         if self.kind == L.RG_DIAG5:
             return self._host_diag[b].copy()
         return self._host_stencil[b, 4].copy()
@@ -318,7 +323,7 @@ class GpuStencilOperator:
     def _full_planes(self):
         if self.kind == L.RG_VAR9:
             return self._host_stencil
-        planes = np.zeros((self.nsets, 9, self.P), dtype=self.np_dtype)
+        planes = np.zeros((self.nsets, 9, self.P), dtype=self.coef_np_dtype)
         inside = _neighbour_mask(self.side)
         for b in range(self.nsets):
             if self.kind == L.RG_CONST9:

@@ -67,10 +67,10 @@ class DeviceSchedule:
         if scales is not None:
             if np.all(scales == scales[:, :1]):
                 self.precond = L.RG_PRECOND_JACOBI_SCALAR
-                self.scale = torch.empty(B, dtype=op.torch_dtype, device=dev)
+                self.scale = torch.empty(B, dtype=op.coef_torch_dtype, device=dev)
             else:
                 self.precond = L.RG_PRECOND_JACOBI_FIELD
-                self.scale = torch.empty((B, op.P), dtype=op.torch_dtype, device=dev)
+                self.scale = torch.empty((B, op.P), dtype=op.coef_torch_dtype, device=dev)
         self.load(sl, scales)
         self.struct = L.rg_sched(L.VARIANT_CODE[self.variant], self.m,
                                  self.omega.data_ptr(), self.alpha.data_ptr(),
@@ -86,7 +86,7 @@ class DeviceSchedule:
             return None
         if any(p is None for p in Ps):
             raise ValueError("mix of preconditioned and unpreconditioned systems in a batch")
-        return np.stack([np.asarray(precond_scale(p, op.P)).astype(op.np_dtype) for p in Ps])
+        return np.stack([np.asarray(precond_scale(p, op.P)).astype(op.coef_np_dtype) for p in Ps])
 
     def key(self):
         return (self.variant, self.m, self.precond)

@@ -246,3 +246,18 @@ def test_torch_inputs_stay_on_device():
     assert isinstance(u, torch.Tensor) and u.is_cuda
     uo, _ = O.solve_stationary(A, f.cpu().numpy(), [0.2, 0.3], tol=1e-300, max_outer=2)
     assert np.array_equal(u.cpu().numpy(), uo)
+
+
+def test_f32_cfg2_hard_system_within_1e5():
+    """cfg2 system 0 (eps 3e-4, the worst-conditioned of the first draws):
+    f32 vectors with f64 arithmetic stay within 1e-5 of the f64 oracle after
+    the full 200 NAG(16) sweeps (pure f32 arithmetic gives 1.4e-5)."""
+    from paper_2412_08076_b200 import configs as CF
+    c = CF.cfg2(batch=1)
+    p, s, f = c["problems"][0], c["schedules"][0], c["F"][0]
+    A = O.assemble_anisotropic(p.epsilon, p.theta, 256)
+    op32 = G.GpuStencilOperator.from_problems([p], dtype=np.float32)
+    u32, rep = G.solve_stationary(op32, f.astype(np.float32), s, tol=1e-300, max_outer=200)
+    uo, ro = O.solve_stationary(A, f, s.omega, s.alpha, variant="nag", tol=1e-300, max_outer=200)
+    assert np.linalg.norm(u32 - uo) <= 1e-5 * np.linalg.norm(uo)
+    assert np.all(np.abs(rep.trace - ro["trace"]) <= 1e-5 * ro["trace"])
