@@ -313,6 +313,23 @@ static int sweep_block(const rg_op* A, const rg_sched* s, int k0, int T, bool ja
     return RG_OK;
 }
 
+// Length of the blocked chunk that starts at step i of an n-step run: n is
+// split into round(n / T) nearly equal chunks (at most 8 steps each), so a
+// 32-step sweep at T=5 runs as 6,6,5,5,5,5 instead of 5,5,5,5,5,5,2.
+static int chunk_len(int n, int T, int i) {
+    int nc = (n + T / 2) / T;
+    if (nc < 1) nc = 1;
+    if (nc < (n + 7) / 8) nc = (n + 7) / 8;
+    const int base = n / nc, rem = n % nc;
+    int start = 0;
+    for (int c = 0; c < nc; ++c) {
+        const int len = base + (c < rem ? 1 : 0);
+        if (i < start + len) return start + len - i;   // steps left in this chunk
+        start += len;
+    }
+    return 1;
+}
+
 // ==================================================================== C ABI
 extern "C" {
 
@@ -471,7 +488,7 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     int k = i0;
     int left = n_steps;
     while (left > 0) {
-        const int t = blocked ? (T < left ? T : left) : 1;
+        const int t = blocked ? chunk_len(n_steps, T, n_steps - left) : 1;
         if (blocked) {
             rc = A->d.dtype == RG_F64
                      ? sweep_block<double>(A, s, k, t, jac, hscale, u[cur], u[cur ^ 1], v[cur], v[cur ^ 1], f, st)
@@ -752,7 +769,7 @@ int rg_solver_step(rg_solver* S, void* stream, int* steps_out) {
     int T = 1;
     int rc;
     if (S->use_block) {
-        T = S->block_T < (m - i) ? S->block_T : (m - i);
+        T = chunk_len(m, S->block_T, i);
         if (S->A->d.dtype == RG_F64) rc = do_block<double>(S, T, boundary_norm ? 1 : 0, st);
         else rc = do_block<float>(S, T, boundary_norm ? 1 : 0, st);
     } else {
