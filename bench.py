@@ -1,12 +1,12 @@
 """Benchmark: batched Jacobi-Richardson(32) sweeps on 1023^2 anisotropic grids.
 
 Workload (BASELINE.json configs[2], the north-star "batched N=1023
-Richardson(m) stencil sweeps"; SURVEY.md §8(d) cfg 3): 8 independent
-anisotropic systems per GPU on 1024x1024 cells (1023^2 unknowns, f64),
-theta ~ U[0, pi], lg eps ~ U[-4, 0], f ~ N(0,1) (rng = default_rng(3), drawn
-per system in that order), weighted Jacobi (relax 2/3), m = 32 Chebyshev
-weights of the Jacobi-scaled operator in Leja order.  Synthetic seeded
-inputs: the reference has no dataset.
+Richardson(m) stencil sweeps"; SURVEY.md §8(d) cfg 3; recipe in
+paper_2412_08076_b200/configs.py:cfg3): 8 independent anisotropic systems per
+GPU on 1024x1024 cells (1023^2 unknowns, f64), theta ~ U[0, pi],
+lg eps ~ U[-4, 0], f ~ N(0,1) (rng = default_rng(3)), weighted Jacobi
+(relax 2/3), m = 32 Chebyshev weights of the Jacobi-scaled operator in Leja
+order.  Synthetic seeded inputs: the reference has no dataset.
 
 One step = one outer sweep (32 inner updates) over all systems of a GPU.
   value     grid-point updates/s, whole job (all ranks), iterates resident in HBM
@@ -50,29 +50,10 @@ MAX_OUTER_TOL = 10_000
 
 
 # ------------------------------------------------------------------ inputs
-def draw_systems(first, count, n=N_SIDE, seed=3):
-    """(eps, theta, f) for systems first..first+count-1 of the global stream."""
-    rng = np.random.default_rng(seed)
-    out = []
-    P = (n - 1) ** 2
-    for b in range(first + count):
-        theta = rng.uniform(0.0, np.pi)
-        eps = 10.0 ** rng.uniform(-4.0, 0.0)
-        f = rng.standard_normal(P)
-        if b >= first:
-            out.append((float(eps), float(theta), f))
-    return out
-
-
-def schedule_for(eps, theta, n=N_SIDE):
-    """Jacobi scale and the Leja-ordered Chebyshev weights of the scaled operator."""
-    from paper_2412_08076_b200.problems import AnisotropicProblem, anisotropic_stencil
-    from paper_2412_08076_b200.schedules import chebyshev_weights, leja_order, stencil_symbol_bounds
-    c = anisotropic_stencil(AnisotropicProblem(eps, theta, n))
-    scale = (2.0 / 3.0) / c[4]          # precond.py:71-77, relax / diag
-    lmax, lmin = stencil_symbol_bounds(c, n)
-    w = leja_order(chebyshev_weights(scale * lmax, scale * lmin, M))
-    return c, scale, w
+def workload(rank):
+    """cfg3 systems rank*8 .. rank*8+7 of the seeded stream (configs.cfg3)."""
+    from paper_2412_08076_b200 import configs
+    return configs.cfg3(first=rank * SYSTEMS_PER_GPU, count=SYSTEMS_PER_GPU, n=N_SIDE, m=M)
 
 
 # ------------------------------------------------------------------ clocks
@@ -125,14 +106,13 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU side
-def _cpu_worker_init(eps, theta, n, seed_f):
+def _cpu_worker_init(eps, theta, n, seed_f, w):
     global _W
     import oracle as O
     A = O.assemble_anisotropic(eps, theta, n)
     f = np.random.default_rng(seed_f).standard_normal(A.shape[0])
     u = np.zeros(A.shape[0])
-    _W = dict(A=A, f=f, u=u, r=f - A.dot(u), scale=O.jacobi_scale(A),
-              w=schedule_for(eps, theta, n)[2], i=0)
+    _W = dict(A=A, f=f, u=u, r=f - A.dot(u), scale=O.jacobi_scale(A), w=w, i=0)
 
 
 def _cpu_worker_steps(k):
@@ -157,12 +137,14 @@ class CpuReference:
     def __init__(self, workers=None, n=N_SIDE):
         import multiprocessing as mp
         self.cores = workers or min(32, len(os.sched_getaffinity(0)))
-        systems = draw_systems(0, min(self.cores, SYSTEMS_PER_GPU), n)
+        wl = workload(0)
         ctx = mp.get_context("fork")
         self.pools = []
         for k in range(self.cores):
-            eps, th, _ = systems[k % len(systems)]
-            self.pools.append(ctx.Pool(1, initializer=_cpu_worker_init, initargs=(eps, th, n, 100 + k)))
+            p = wl["problems"][k % len(wl["problems"])]
+            w = wl["schedules"][k % len(wl["problems"])].omega
+            self.pools.append(ctx.Pool(1, initializer=_cpu_worker_init,
+                                       initargs=(p.epsilon, p.theta, n, 100 + k, w)))
         self.n = n
         for p in self.pools:   # wait for assembly
             p.apply(_cpu_worker_steps, (0,))
@@ -251,15 +233,10 @@ def run_gpu(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    systems = draw_systems(rank * SYSTEMS_PER_GPU, SYSTEMS_PER_GPU)
-    probs, scheds, scales = [], [], []
-    for eps, th, _ in systems:
-        c, sc, w = schedule_for(eps, th)
-        probs.append(G.AnisotropicProblem(eps, th, N_SIDE))
-        scheds.append(G.WeightSchedule(omega=w))
-        scales.append(sc)
+    wl = workload(rank)
+    probs, scheds, scales = wl["problems"], wl["schedules"], wl["scales"]
     op = G.GpuStencilOperator.from_problems(probs, dtype=np.float64, device=dev)
-    F = np.stack([f for _, _, f in systems])
+    F = wl["F"]
     P = [G.JacobiScale(np.float64(s)) for s in scales]
     B, Pn = op.batch, op.P
 

@@ -12,7 +12,8 @@ oracle then consume identically.
   cfg2  NAG(16), 64 x 255^2, (lg eps, theta) random, random-init GELU MLP
         3x64 -> 32 (omega = softplus, alpha = sigmoid), 200 outer; f64 and f32.
   cfg3  Jacobi Richardson(32), 8 x 1023^2, Leja-ordered Chebyshev of the
-        scaled operator (symbol bounds); to 1e-6.
+        scaled operator (lambda_max: symbol maximum; lambda_min: small-grid
+        eigenvalues extrapolated in h^2, x0.9); to 1e-6.
   cfg4  FNS: 4 x 1023^2, eps=1e-3, symbol from a random-init 4-layer conv net
         on the sine-frequency grid (x0.01), M = 8 smoothing steps omega=0.5;
         100 alternations.
@@ -27,7 +28,8 @@ import numpy as np
 import torch
 
 from .problems import AnisotropicProblem, HelmholtzProblem, anisotropic_stencil
-from .schedules import WeightSchedule, chebyshev_weights, leja_order, stencil_symbol_bounds
+from .schedules import (WeightSchedule, chebyshev_weights, leja_order, stencil_lambda_min,
+                        stencil_symbol_bounds)
 
 ANISOTROPIC_BOUNDS = np.array([[-6.0, 0.0], [0.0, np.pi]])  # metanet.py:24 (lg eps, theta)
 
@@ -130,7 +132,8 @@ def cfg3(first=0, count=8, n=1024, m=32, seed=3):
         p = AnisotropicProblem(float(eps), float(theta), n)
         c = anisotropic_stencil(p)
         sc = (2.0 / 3.0) / c[4]                  # weighted Jacobi, relax 2/3 (precond.py:71-77)
-        lmax, lmin = stencil_symbol_bounds(c, n)
+        lmax = stencil_symbol_bounds(c, n)[0]
+        lmin = stencil_lambda_min(c, n)
         probs.append(p)
         F.append(f)
         scheds.append(WeightSchedule(omega=leja_order(chebyshev_weights(sc * lmax, sc * lmin, m))))

@@ -301,7 +301,7 @@ def solve_stationary(A, f, schedule, P=None, tol=1e-6, max_outer=100_000, u0=Non
     if op.batch != 1:
         raise DimensionMismatch("use solve_stationary_batched for a batched operator")
     _check_len(op, f)
-    S = StationarySolver(op, schedule, P, tol, max_outer, check, block_T)
+    S = StationarySolver.cached(op, schedule, P, tol, max_outer, check, block_T)
     S.begin(f, u0)
     S.run()
     u, rep = S.result(0, like_numpy=_is_host(f))

@@ -117,3 +117,47 @@ def stencil_symbol_bounds(coeffs, n, grid=721):
     lmax = float(np.max(sigma(xi, eta)))
     lmin = float(min(sigma(np.pi / n, np.pi / n), sigma(np.pi / n, -np.pi / n)))
     return lmax, lmin
+
+
+def stencil_matrix(coeffs, side):
+    """Host CSR of a constant 9-point stencil on a side x side interior
+    (CSR column order, zero-padded at the Dirichlet boundary)."""
+    import scipy.sparse as sp
+    c = np.asarray(coeffs, dtype=float).reshape(3, 3)
+    idx = np.arange(side * side).reshape(side, side)
+    rows, cols, vals = [], [], []
+    for a in (-1, 0, 1):
+        for b in (-1, 0, 1):
+            if c[a + 1, b + 1] == 0.0:
+                continue
+            i0, i1 = max(0, -a), min(side, side - a)
+            j0, j1 = max(0, -b), min(side, side - b)
+            r = idx[i0:i1, j0:j1]
+            rows.append(r.reshape(-1))
+            cols.append((r + a * side + b).reshape(-1))
+            vals.append(np.full(r.size, c[a + 1, b + 1]))
+    n = side * side
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(n, n))
+
+
+def stencil_lambda_min(coeffs, n, grids=(64, 128), safety=0.9):
+    """lambda_min of the stencil on the n-cell grid, extrapolated from exact
+    small-grid eigenvalues: the unscaled FEM stiffness has lambda_min(n) ~
+    mu / n^2 with an O(h^2) error, so mu is Richardson-extrapolated from
+    n = grids[0], grids[1] and a safety factor keeps the estimate below the
+    true value.  (The symbol value at the lowest Dirichlet frequency can
+    miss the rotated operator's lambda_min by 10x or more.)"""
+    import scipy.sparse.linalg as sla
+    mu = []
+    for g in grids:
+        if g >= n:
+            g = n
+        A = stencil_matrix(coeffs, g - 1)
+        lam = sla.eigsh(A, k=1, sigma=0, which="LM", return_eigenvectors=False)[0]
+        mu.append(lam * g * g)
+    if grids[1] >= n:
+        return safety * mu[1] / (n * n)
+    r = (grids[1] / grids[0]) ** 2
+    ext = (r * mu[1] - mu[0]) / (r - 1)
+    return safety * min(ext, mu[1]) / (n * n)

@@ -9,6 +9,6 @@ mkdir -p gpurun_out
 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:block_kernel -s ${NCU_SKIP:-30} -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:block_kernel -s ${NCU_SKIP:-30} -c ${NCU_COUNT:-1} \
     -o gpurun_out/prof_block $CMD > gpurun_out/ncu_full.log 2>&1
 echo done
