@@ -130,21 +130,34 @@ class JacobiScale:
         return self.scale * np.asarray(r)
 
 
+_SCALE_MEMO = {}
+
+
 def precond_scale(P, n):
-    """Scale array of a Jacobi-type preconditioner (ours or richlab's), None
-    for P=None.  richlab hides the scale in a closure; P.apply(ones) returns
-    it exactly (scale * 1.0 == scale)."""
+    """Jacobi scale of a preconditioner (ours or richlab's): a 0-d array when
+    it is one constant, else a length-n array; None for P=None.  richlab
+    hides the scale in a closure; P.apply(ones) returns it exactly
+    (scale * 1.0 == scale).  Results are memoised per preconditioner object."""
     if P is None:
         return None
+    key = (id(P), n)
+    hit = _SCALE_MEMO.get(key)
+    if hit is not None and hit[0] is P:
+        return hit[1]
     if isinstance(P, JacobiScale):
         s = P.scale
-        return np.broadcast_to(s, (n,)) if s.ndim == 0 else s
-    kind = getattr(P, "kind", None)
-    if kind in ("weighted-jacobi", "identity"):
-        return np.asarray(P.apply(np.ones(n)))
-    raise UnsupportedOperator(
-        f"preconditioner kind {kind!r} has no GPU path (weighted Jacobi only; "
-        "GS/SOR/SSOR are SURVEY.md §8(f) next items)")
+    elif getattr(P, "kind", None) in ("weighted-jacobi", "identity"):
+        s = np.asarray(P.apply(np.ones(n)))
+    else:
+        raise UnsupportedOperator(
+            f"preconditioner kind {getattr(P, 'kind', None)!r} has no GPU path (weighted "
+            "Jacobi only; GS/SOR/SSOR are SURVEY.md §8(f) next items)")
+    if s.ndim == 1 and s.size and np.all(s == s[0]):
+        s = np.asarray(s[0])
+    if len(_SCALE_MEMO) > 256:
+        _SCALE_MEMO.clear()
+    _SCALE_MEMO[key] = (P, s)
+    return s
 
 
 def as_numpy_dtype(dt):

@@ -65,7 +65,7 @@ class DeviceSchedule:
         self.precond = L.RG_PRECOND_NONE
         self.scale = None
         if scales is not None:
-            if np.all(scales == scales[:, :1]):
+            if scales.shape[1] == 1:
                 self.precond = L.RG_PRECOND_JACOBI_SCALAR
                 self.scale = torch.empty(B, dtype=op.coef_torch_dtype, device=dev)
             else:
@@ -86,7 +86,10 @@ class DeviceSchedule:
             return None
         if any(p is None for p in Ps):
             raise ValueError("mix of preconditioned and unpreconditioned systems in a batch")
-        return np.stack([np.asarray(precond_scale(p, op.P)).astype(op.coef_np_dtype) for p in Ps])
+        sc = [precond_scale(p, op.P) for p in Ps]
+        if all(x.ndim == 0 for x in sc):          # one constant per system: [B, 1]
+            return np.array([[x] for x in sc], dtype=op.coef_np_dtype)
+        return np.stack([np.broadcast_to(x, (op.P,)) for x in sc]).astype(op.coef_np_dtype)
 
     def key(self):
         return (self.variant, self.m, self.precond)
@@ -110,8 +113,7 @@ class DeviceSchedule:
             return None
         scales = self._scales(P)
         kind = L.RG_PRECOND_NONE if scales is None else (
-            L.RG_PRECOND_JACOBI_SCALAR if np.all(scales == scales[:, :1])
-            else L.RG_PRECOND_JACOBI_FIELD)
+            L.RG_PRECOND_JACOBI_SCALAR if scales.shape[1] == 1 else L.RG_PRECOND_JACOBI_FIELD)
         return (sl, scales) if kind == self.precond else None
 
 
