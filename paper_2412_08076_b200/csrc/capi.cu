@@ -15,6 +15,7 @@
 #include "block.cuh"
 #include "dst.cuh"
 #include "mg.cuh"
+#include "small.cuh"
 
 using namespace rg;
 
@@ -59,6 +60,7 @@ struct rg_solver {
     int check;
     int block_T;
     bool use_block;
+    bool use_small;   // whole solve in one launch (grid fits in shared memory)
     SysState* d_st;
     double* d_trace;
     double* d_part;
@@ -660,6 +662,14 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     // automatic depth: measured optimum on B200 for the 64x64 tile (profiles/)
     S->block_T = block_T != 0 ? block_T : (s->variant >= RG_NAG ? 6 : 5);
     if (!S->use_block) S->block_T = 1;
+    {
+        const size_t smem = A->d.dtype == RG_F32 ? small_smem_bytes<float>(A->d.side, s->variant)
+                                                 : small_smem_bytes<double>(A->d.side, s->variant);
+        S->use_small = real && A->d.kind == RG_CONST9 && block_T == 0 &&
+                       s->precond != RG_PRECOND_JACOBI_FIELD &&
+                       (long long)A->d.side * A->d.side <= (long long)SMALL_NT * SMALL_PPT &&
+                       smem <= 200 * 1024;
+    }
     S->kmax = (long long)max_outer * s->m;
     const dim3 g = step_grid(A);
     int cap = g.x * g.y;
@@ -742,6 +752,10 @@ int rg_solver_begin(rg_solver* S, void* u0, void* u1, void* v0, void* v1, const 
     CUDA_TRY(cudaMemsetAsync(S->d_st, 0, sizeof(SysState) * A->d.batch, st));
     CUDA_TRY(cudaMemsetAsync(S->d_trace, 0, sizeof(double) * A->d.batch * (size_t)S->trace_stride, st));
     if (v0) CUDA_TRY(cudaMemsetAsync(v0, 0, vbytes, st));  // v = 0 at entry (:95)
+    if (S->use_small) {   // the single-launch solver computes ||f|| and trace[0] itself
+        S->begun = true;
+        return RG_OK;
+    }
     StepReq q;
     memset(&q, 0, sizeof q);
     q.u_in = u0;
@@ -763,6 +777,39 @@ int rg_solver_step(rg_solver* S, void* stream, int* steps_out) {
     if (S->k >= S->kmax) return RG_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int m = S->s.m;
+    if (S->use_small) {   // the whole remaining solve in one launch
+        const rg_op* A = S->A;
+        cudaError_t err;
+        if (A->d.dtype == RG_F64) {
+            SmallArgs<double> a;
+            a.coef = (const double*)A->d.stencil;
+            a.scale = S->s.precond == RG_PRECOND_JACOBI_SCALAR ? (const double*)S->s.scale : nullptr;
+            a.u = (double*)S->u[0];
+            a.f = (const double*)S->f;
+            a.omega = S->s.omega; a.alpha = S->s.alpha; a.atil = S->s.alpha_tilde;
+            a.side = A->d.side; a.P = A->P; a.m = m; a.shared = A->d.shared; a.cfg = S->cfg;
+            a.st = S->d_st; a.trace = S->d_trace; a.trace_stride = S->trace_stride;
+            err = launch_small<double>(a, S->s.variant >= RG_NAG ? V_NAG : S->s.variant,
+                                       a.scale != nullptr, A->d.batch, st);
+        } else {
+            SmallArgs<float> a;
+            a.coef = (const double*)A->d.stencil;
+            a.scale = S->s.precond == RG_PRECOND_JACOBI_SCALAR ? (const double*)S->s.scale : nullptr;
+            a.u = (float*)S->u[0];
+            a.f = (const float*)S->f;
+            a.omega = S->s.omega; a.alpha = S->s.alpha; a.atil = S->s.alpha_tilde;
+            a.side = A->d.side; a.P = A->P; a.m = m; a.shared = A->d.shared; a.cfg = S->cfg;
+            a.st = S->d_st; a.trace = S->d_trace; a.trace_stride = S->trace_stride;
+            err = launch_small<float>(a, S->s.variant >= RG_NAG ? V_NAG : S->s.variant,
+                                      a.scale != nullptr, A->d.batch, st);
+        }
+        if (err != cudaSuccess) return fail(RG_ECUDA, "small solve launch: %s", cudaGetErrorString(err));
+        if (steps_out) *steps_out = (int)(S->kmax - S->k);
+        S->k = S->kmax;
+        S->launches += 1;
+        S->need_flush = false;
+        return RG_OK;
+    }
     const int i = (int)(S->k % m);
     const bool nag = S->s.variant >= RG_NAG;
     const bool boundary_norm = nag && i == 0 && S->k > 0 && S->flushed_k != S->k;
