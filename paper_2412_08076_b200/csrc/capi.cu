@@ -61,6 +61,7 @@ struct rg_solver {
     int block_T;
     bool use_block;
     bool use_small;   // whole solve in one launch (grid fits in shared memory)
+    bool small_done;  // that launch has been queued
     SysState* d_st;
     double* d_trace;
     double* d_part;
@@ -753,6 +754,7 @@ int rg_solver_begin(rg_solver* S, void* u0, void* u1, void* v0, void* v1, const 
     CUDA_TRY(cudaMemsetAsync(S->d_trace, 0, sizeof(double) * A->d.batch * (size_t)S->trace_stride, st));
     if (v0) CUDA_TRY(cudaMemsetAsync(v0, 0, vbytes, st));  // v = 0 at entry (:95)
     if (S->use_small) {   // the single-launch solver computes ||f|| and trace[0] itself
+        S->small_done = false;
         S->begun = true;
         return RG_OK;
     }
@@ -774,10 +776,10 @@ int rg_solver_step(rg_solver* S, void* stream, int* steps_out) {
     if (!S) return fail(RG_ENULL, "null solver");
     if (!S->begun) return fail(RG_ESTATE, "rg_solver_begin not called");
     if (steps_out) *steps_out = 0;
-    if (S->k >= S->kmax) return RG_OK;
+    if (S->use_small ? S->small_done : S->k >= S->kmax) return RG_OK;
     cudaStream_t st = (cudaStream_t)stream;
     const int m = S->s.m;
-    if (S->use_small) {   // the whole remaining solve in one launch
+    if (S->use_small) {   // the whole solve (even max_outer = 0) in one launch
         const rg_op* A = S->A;
         cudaError_t err;
         if (A->d.dtype == RG_F64) {
@@ -806,6 +808,7 @@ int rg_solver_step(rg_solver* S, void* stream, int* steps_out) {
         if (err != cudaSuccess) return fail(RG_ECUDA, "small solve launch: %s", cudaGetErrorString(err));
         if (steps_out) *steps_out = (int)(S->kmax - S->k);
         S->k = S->kmax;
+        S->small_done = true;
         S->launches += 1;
         S->need_flush = false;
         return RG_OK;
@@ -879,6 +882,12 @@ int rg_solver_run(rg_solver* S, int n_sweeps, void* stream) {
     const long long m = S->s.m;
     long long target = (S->k / m + n_sweeps) * m;
     if (target > S->kmax) target = S->kmax;
+    if (S->use_small) {
+        int steps = 0;
+        int rc = rg_solver_step(S, stream, &steps);
+        if (rc) return rc;
+        return RG_OK;
+    }
     while (S->k < target) {
         int steps = 0;
         int rc = rg_solver_step(S, stream, &steps);
@@ -897,7 +906,7 @@ int rg_solver_poll(rg_solver* S, void* stream, int* n_active, int* done) {
     int act = 0;
     for (int b = 0; b < B; ++b) act += S->h_st[b].status == ST_ACTIVE;
     if (n_active) *n_active = act;
-    if (done) *done = (act == 0) || (S->k >= S->kmax && !S->need_flush);
+    if (done) *done = (act == 0) || (S->use_small ? S->small_done : (S->k >= S->kmax && !S->need_flush));
     return RG_OK;
 }
 
