@@ -76,7 +76,7 @@ struct BlockArgs {
 template <typename S, int VAR>
 struct BlockMinCtas {
     static constexpr int value = (RG_BLK_LR * 64 * 16 > 100 * 1024) ? 1
-                                 : ((VAR == V_PLAIN) ? RG_MINB_PLAIN_F64 : (VAR == V_MOM ? 2 : 1));
+                                 : ((VAR == V_PLAIN) ? RG_MINB_PLAIN_F64 : 2);
 };
 
 // Tile shape used by the library (load window LR x LC, NW warps).
@@ -109,6 +109,10 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
     typedef C Row[LC];
     Row* buf0 = reinterpret_cast<Row*>(smem_raw);
     Row* buf1 = buf0 + LR;
+    // nag keeps f in shared memory (u, v stay in registers) so that two CTAs
+    // fit per SM; plain/mom keep f in registers
+    constexpr bool F_SMEM = NAG;
+    Row* sf = buf1 + LR;
 
     const int bl = blockIdx.y;          // system within this launch
     const int b = a.b0 + bl;            // global system index
@@ -141,7 +145,9 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
             const bool in = (gx >= 0) && (gx < side) && (gy >= 0) && (gy < side);
             const size_t g = base + (size_t)gx * side + gy;
             const C u = in ? to_c(a.u_in[g]) : szero<C>();
-            fr[rr][cc] = in ? to_c(a.f[g]) : szero<C>();
+            const C fv = in ? to_c(a.f[g]) : szero<C>();
+            if (F_SMEM) sf[r0 + rr][col] = fv;
+            else fr[rr][cc] = fv;
             vr[rr][cc] = (HASV && in) ? to_c(a.v_in[g]) : szero<C>();
             if (NAG) ur[rr][cc] = u;
             if (in) dom |= 1u << (rr * CPT + cc);
@@ -218,7 +224,8 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
     if (NAG && a.norm_first_u) {
         // residual at u itself for the sweep-boundary convergence test (:124-125)
         sweep_rows(buf1, [&](int rr, int cc, int r, int col, C s, C) {
-            const C rs = (owned(r, col) && indom(rr, cc)) ? sub(fr[rr][cc], s) : szero<C>();
+            const C fv = F_SMEM ? sf[r][col] : fr[rr][cc];
+            const C rs = (owned(r, col) && indom(rr, cc)) ? sub(fv, s) : szero<C>();
             acc[0] = sqacc(acc[0], rs);
         });
         __syncthreads();
@@ -240,7 +247,8 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
             const bool last = (t == T - 1);
             sweep_rows(cur, [&](int rr, int cc, int r, int col, C s, C centre) {
                 const bool live = INTERIOR || indom(rr, cc);
-                const C rs = sub(fr[rr][cc], s);                        // r = f - A x
+                const C fv = F_SMEM ? sf[r][col] : fr[rr][cc];
+                const C rs = sub(fv, s);                                // r = f - A x
                 if (!NAG && a.norm_every) {
                     const C rn = (live && owned(r, col)) ? rs : szero<C>();
                     acc[(NACC > 1) ? t : 0] = sqacc(acc[(NACC > 1) ? t : 0], rn);
@@ -279,7 +287,7 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
 template <typename S, int VAR, int T, bool JAC>
 cudaError_t launch_block_t(const BlockArgs<S>& a, int nsys, cudaStream_t st) {
     auto kern = block_kernel<S, VAR, T, BLK_LR, BLK_LC, BLK_NW, JAC>;
-    const size_t smem = 2 * (size_t)BLK_LR * BLK_LC * sizeof(CT<S>);
+    const size_t smem = (VAR >= V_NAG ? 3 : 2) * (size_t)BLK_LR * BLK_LC * sizeof(CT<S>);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -487,7 +487,7 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
         CUDA_TRY(cudaMemcpyAsync(hscale.data(), s->scale, B * sizeof(double), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
     }
-    const int T = block_T == 0 ? (s->variant >= RG_NAG ? 6 : 5) : block_T;
+    const int T = block_T == 0 ? 5 : block_T;
     int k = i0;
     int left = n_steps;
     while (left > 0) {
@@ -661,7 +661,7 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     S->use_block = real && A->d.kind == RG_CONST9 && check == RG_CHECK_OUTER &&
                    s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
     // automatic depth: measured optimum on B200 for the 64x64 tile (profiles/)
-    S->block_T = block_T != 0 ? block_T : (s->variant >= RG_NAG ? 6 : 5);
+    S->block_T = block_T != 0 ? block_T : 5;
     if (!S->use_block) S->block_T = 1;
     {
         const size_t smem = A->d.dtype == RG_F32 ? small_smem_bytes<float>(A->d.side, s->variant)

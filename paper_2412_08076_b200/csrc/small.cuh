@@ -110,7 +110,10 @@ __global__ void __launch_bounds__(SMALL_NT, 1) small_solve_kernel(SmallArgs<S> a
         }
         return acc;
     };
-    SysState& S_ = a.st[b];
+    // the decision state lives in shared memory for the whole solve (thread 0
+    // updates it between two barriers every step); copied back at the end
+    __shared__ SysState S_;
+    if (tid == 0) S_ = a.st[b];
     double* trace = a.trace + (size_t)b * a.trace_stride;
 
     // ||f|| and the initial residual (:96-110)
@@ -166,6 +169,7 @@ __global__ void __launch_bounds__(SMALL_NT, 1) small_solve_kernel(SmallArgs<S> a
             __syncthreads();
         }
     }
+    if (tid == 0) a.st[b] = S_;
     if (S_.status != ST_DIVERGED) {
 #pragma unroll
         for (int j = 0; j < SMALL_PPT; ++j) {
