@@ -34,20 +34,19 @@ struct SmallArgs {
     int trace_stride;
 };
 
-// Sum over the CTA, result broadcast to every thread (2 barriers).
-__device__ inline double small_sum(double v, double* red) {
+// Sum over the CTA, returned to EVERY thread with identical bits: each warp
+// reduces the 32 per-warp partials in the same fixed tree order, so all
+// threads can take the convergence decision themselves (one barrier).
+__device__ inline double small_sum_all(double v, double* red) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if (lane == 0) red[w] = v;
     __syncthreads();
-    double t = 0.0;
-    if (w == 0) {
-        t = red[lane];                          // 32 warps
+    double t = red[lane];                       // 32 warps
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
-    }
-    return t;                                   // valid in thread 0
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    return __shfl_sync(0xffffffffu, t, 0);
 }
 
 template <typename S, int VAR, bool JAC>
@@ -57,7 +56,6 @@ __global__ void __launch_bounds__(SMALL_NT, 1) small_solve_kernel(SmallArgs<S> a
     constexpr bool HASV = VAR != V_PLAIN;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ double red[32];
-    __shared__ int status;
     const int b = blockIdx.x;
     const int s = a.side, W = s + 2, P = a.P, m = a.m;
     C* U = reinterpret_cast<C*>(smem_raw);      // [(s+2)^2], zero border
@@ -110,27 +108,32 @@ __global__ void __launch_bounds__(SMALL_NT, 1) small_solve_kernel(SmallArgs<S> a
         }
         return acc;
     };
-    // the decision state lives in shared memory for the whole solve (thread 0
-    // updates it between two barriers every step); copied back at the end
-    __shared__ SysState S_;
-    if (tid == 0) S_ = a.st[b];
     double* trace = a.trace + (size_t)b * a.trace_stride;
+    const SolveCfg cf = a.cfg;
 
-    // ||f|| and the initial residual (:96-110)
+    // ||f|| and the initial residual (:96-110); every thread holds the same
+    // decision state (identical reductions), thread 0 writes trace / state.
+    int status = ST_ACTIVE, outer = 0, inner = 0;
+    double fnorm, trace0, rel, bad_rel = 0.0;
     {
         double ff = 0.0;
 #pragma unroll
         for (int j = 0; j < SMALL_PPT; ++j) ff = sqacc(ff, fr[j]);
-        const double r2 = small_sum(residual_u(), red);
+        const double r2 = small_sum_all(residual_u(), red);
         __syncthreads();
-        const double f2 = small_sum(ff, red);
-        if (tid == 0) {
-            double tot[1] = {r2};
-            finalize(S_, trace, a.cfg, 0, 1, tot, 1, f2, 0);
-            status = S_.status;
+        const double f2 = small_sum_all(ff, red);
+        fnorm = sqrt(f2);
+        if (fnorm == 0.0) {                                 // :97-100
+            status = ST_CONVERGED; rel = 0.0; trace0 = 0.0;
+        } else {
+            rel = sqrt(r2) / fnorm;
+            trace0 = rel;
+            if (rel <= cf.tol) status = ST_CONVERGED;
+            else if (cf.max_outer <= 0) status = ST_MAXED;
         }
-        __syncthreads();
+        if (tid == 0) trace[0] = trace0;
     }
+    const double div_thr = cf.div_factor * fmax(trace0, 1.0);
     int k = 0;
     while (status == ST_ACTIVE) {
         const int i = k % m;
@@ -158,19 +161,35 @@ __global__ void __launch_bounds__(SMALL_NT, 1) small_solve_kernel(SmallArgs<S> a
         }
         __syncthreads();
         ++k;
-        const bool test = !NAG || a.cfg.check_inner || (k % m) == 0;   // (:123)
+        const bool test = !NAG || cf.check_inner || (k % m) == 0;   // (:123)
         if (test) {
-            const double r2 = small_sum(residual_u(), red);
-            if (tid == 0) {
-                double tot[1] = {r2};
-                finalize(S_, trace, a.cfg, k, 1, tot, 0, 0.0, 0);
-                status = S_.status;
+            const double r2 = small_sum_all(residual_u(), red);
+            rel = sqrt(r2) / fnorm;
+            inner = k;
+            const bool boundary = (k % m) == 0;
+            if (!isfinite(rel) || rel > div_thr) {                 // :126-129
+                status = ST_DIVERGED; bad_rel = rel;
+            } else {
+                if (boundary) {                                    // :133-134
+                    outer = k / m;
+                    if (tid == 0) trace[outer] = rel;
+                }
+                if ((cf.check_inner || boundary) && rel <= cf.tol) {   // :130-136
+                    status = ST_CONVERGED;
+                    if (!boundary) { outer = k / m + 1; if (tid == 0) trace[outer] = rel; }
+                } else if (boundary && outer >= cf.max_outer) {
+                    status = ST_MAXED;
+                }
             }
-            __syncthreads();
         }
     }
-    if (tid == 0) a.st[b] = S_;
-    if (S_.status != ST_DIVERGED) {
+    if (tid == 0) {
+        SysState& st = a.st[b];
+        st.fnorm = fnorm; st.trace0 = trace0; st.rel = rel; st.bad_rel = bad_rel;
+        st.status = status; st.outer = outer; st.inner = inner; st.ans_buf = 0;
+        st.last_j = k;
+    }
+    if (status != ST_DIVERGED) {
 #pragma unroll
         for (int j = 0; j < SMALL_PPT; ++j) {
             const int p = tid + j * SMALL_NT;
