@@ -165,17 +165,43 @@ class GpuHierarchy:
         L.check(lib.rg_prolong_add(lvl.op.rg_dtype, self.batch, lvl.n, L.ptr(ec), L.ptr(u), s))
         return self._smooth(k, f, u, post)
 
+    use_graphs = True
+
+    def _cycle(self, zero_u, pre, post):
+        ud = self._buf("ua", 0)
+        if zero_u:
+            ud.zero_()
+        return self._level(0, self._buf("f", 0), ud, pre, post)
+
     def apply(self, f, u=None, pre=1, post=1):
-        """One V-cycle on device tensors f, u [batch, P0]; returns a new tensor."""
-        op0 = self.levels[0].op
+        """One V-cycle on device tensors f, u [batch, P0]; returns a new tensor.
+
+        The ~200 launches of a cycle (smoother steps, residuals, transfers on
+        7 levels) are captured once into a CUDA graph per (u given, pre,
+        post) and replayed: the inputs are copied into the hierarchy's fixed
+        buffers first, so every replay sees the same pointers."""
         fd = self._buf("f", 0)
         fd.copy_(f.reshape(fd.shape))
-        ud = self._buf("ua", 0)
-        if u is None:
-            ud.zero_()
+        if u is not None:
+            self._buf("ua", 0).copy_(u.reshape(fd.shape))
+        key = (u is None, pre, post)
+        graphs = self.__dict__.setdefault("_graphs", {})
+        if self.use_graphs and key not in graphs:
+            self._cycle(u is None, pre, post)            # eager warm-up: buffers, attributes
+            if u is not None:
+                self._buf("ua", 0).copy_(u.reshape(fd.shape))
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    out_g = self._cycle(u is None, pre, post)
+                graphs[key] = (g, out_g)
+            except Exception:  # noqa: BLE001  capture unsupported here: stay eager
+                self.use_graphs = False
+        if self.use_graphs and key in graphs:
+            g, out = graphs[key]
+            g.replay()
         else:
-            ud.copy_(u.reshape(ud.shape))
-        out = self._level(0, fd, ud, pre, post)
+            out = self._cycle(u is None, pre, post)
         res = out.clone()
         if not bool(torch.isfinite(res).all()):
             m = self.levels[0].sched.m if self.levels[0].sched is not None else 0
