@@ -35,27 +35,55 @@ struct DstArgs {
 };
 enum { DST_PLAIN = 0, DST_TWICE_LAM = 1, DST_ADD = 2 };
 
+__device__ __forceinline__ double2 cmul_conj_tw(double2 b, double2 c) {
+    // b * w with w = (c.x, -c.y) = exp(-i theta), c = (cos, sin)(theta)
+    return make_double2(fma(b.x, c.x, b.y * c.y), fma(b.y, c.x, -b.x * c.y));
+}
+
 // One complex radix-2 DIT FFT of length M on z (bit-reversed input order),
 // executed cooperatively by the CTA on `nl` lines stored back to back.
+// Stages are fused in pairs (radix-2^2): a thread loads the 4 elements
+// {i, i+h, i+2h, i+3h}, applies the two butterfly stages (half sizes h and
+// 2h) in registers and stores once -- half the shared-memory passes and
+// barriers of plain radix-2.  An odd log2(M) leaves one radix-2 stage.
+// Twiddle of stage half-size h at offset j: exp(-i pi j / h) = tw[j * M / h].
 __device__ inline void fft_lines(double2* z, int nl, int M, int logM, const double2* tw) {
-    const int nb = nl * (M >> 1);   // butterflies per pass over all lines
-    for (int s = 1; s <= logM; ++s) {
-        const int half = 1 << (s - 1);
-        const int tstride = M >> s;     // twiddle index step: e^{-2 pi i j / 2half} = tw[j * M/half / 2 * 2]
+    int s = 1;
+    if (logM & 1) {                       // one radix-2 stage (h = 1, twiddle 1)
+        const int nb = nl * (M >> 1);
         for (int t = threadIdx.x; t < nb; t += blockDim.x) {
-            const int line = t / (M >> 1);
-            const int bt = t - line * (M >> 1);
-            const int grp = bt >> (s - 1);
-            const int j = bt & (half - 1);
-            const int i0 = line * M + grp * 2 * half + j;
-            const int i1 = i0 + half;
-            // w = exp(-2 pi i j / (2 half)) = exp(-i pi (j * M / half) / M)
-            const double2 c = tw[j * tstride * 2];
-            const double2 a = z[i0], bq = z[i1];
-            // bq * w, w = (c.x, -c.y)
-            const double2 p = make_double2(fma(bq.x, c.x, bq.y * c.y), fma(bq.y, c.x, -bq.x * c.y));
-            z[i0] = make_double2(a.x + p.x, a.y + p.y);
-            z[i1] = make_double2(a.x - p.x, a.y - p.y);
+            const int i0 = 2 * t;         // lines are contiguous, M even
+            const double2 a = z[i0], b = z[i0 + 1];
+            z[i0] = make_double2(a.x + b.x, a.y + b.y);
+            z[i0 + 1] = make_double2(a.x - b.x, a.y - b.y);
+        }
+        __syncthreads();
+        s = 2;
+    }
+    for (; s < logM; s += 2) {
+        const int h = 1 << (s - 1);       // first stage half-size; second is 2h
+        const int nq = nl * (M >> 2);     // 4-element groups over all lines
+        for (int t = threadIdx.x; t < nq; t += blockDim.x) {
+            const int line = t / (M >> 2);
+            const int g = t - line * (M >> 2);
+            const int blk = g / h, j = g - blk * h;
+            const int i0 = line * M + blk * 4 * h + j;
+            double2 x0 = z[i0], x1 = z[i0 + h], x2 = z[i0 + 2 * h], x3 = z[i0 + 3 * h];
+            // stage s: pairs (x0,x1), (x2,x3) with exp(-i pi j / h)
+            const double2 w1 = __ldg(&tw[j * (M / h)]);
+            double2 p = cmul_conj_tw(x1, w1);
+            double2 q = cmul_conj_tw(x3, w1);
+            double2 a0 = make_double2(x0.x + p.x, x0.y + p.y), a1 = make_double2(x0.x - p.x, x0.y - p.y);
+            double2 a2 = make_double2(x2.x + q.x, x2.y + q.y), a3 = make_double2(x2.x - q.x, x2.y - q.y);
+            // stage s+1: pairs (a0,a2) with exp(-i pi j / 2h), (a1,a3) with exp(-i pi (j+h) / 2h)
+            const double2 w2 = __ldg(&tw[j * (M / (2 * h))]);
+            const double2 w3 = __ldg(&tw[(j + h) * (M / (2 * h))]);
+            p = cmul_conj_tw(a2, w2);
+            q = cmul_conj_tw(a3, w3);
+            z[i0] = make_double2(a0.x + p.x, a0.y + p.y);
+            z[i0 + 2 * h] = make_double2(a0.x - p.x, a0.y - p.y);
+            z[i0 + h] = make_double2(a1.x + q.x, a1.y + q.y);
+            z[i0 + 3 * h] = make_double2(a1.x - q.x, a1.y - q.y);
         }
         __syncthreads();
     }
