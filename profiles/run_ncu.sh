@@ -4,7 +4,7 @@
 #   2. the launch list of the same command (cold-cache, serialised: compare shares),
 #   3. one `--set full` capture of the dominant kernel (temporally blocked sweep).
 set -u
-CMD="python bench.py --steps 4 --warmup 3 --no-cpu --no-time-to-tol --e2e-steps 1 ${BENCH_ARGS:-}"
+CMD="python bench.py --steps 4 --warmup 3 --no-cpu --e2e-steps 0 ${BENCH_ARGS:-}"
 mkdir -p gpurun_out
 $CMD > gpurun_out/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
