@@ -15,7 +15,7 @@
 #include "block.cuh"
 #include "dst.cuh"
 #include "mg.cuh"
-#include "small.cuh"
+#include "cluster.cuh"
 
 using namespace rg;
 
@@ -62,6 +62,7 @@ struct rg_solver {
     bool use_block;
     bool use_small;   // whole solve in one launch (grid fits in shared memory)
     bool small_done;  // that launch has been queued
+    int cl_nc, cl_rows, cl_ppt;   // cluster shape of the resident solver
     SysState* d_st;
     double* d_trace;
     double* d_part;
@@ -664,12 +665,18 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     S->block_T = block_T != 0 ? block_T : 5;
     if (!S->use_block) S->block_T = 1;
     {
-        const size_t smem = A->d.dtype == RG_F32 ? small_smem_bytes<float>(A->d.side, s->variant)
-                                                 : small_smem_bytes<double>(A->d.side, s->variant);
-        S->use_small = real && A->d.kind == RG_CONST9 && block_T == 0 &&
-                       s->precond != RG_PRECOND_JACOBI_FIELD &&
-                       (long long)A->d.side * A->d.side <= (long long)SMALL_NT * SMALL_PPT &&
-                       smem <= 200 * 1024;
+        // resident cluster solver: the whole solve in one launch when the grid
+        // fits in the distributed shared memory of <= 16 CTAs
+        int nc = 0, rows = 0, ppt = 0;
+        cluster_shape(A->d.side, &nc, &rows, &ppt);
+        const int v = s->variant >= RG_NAG ? V_NAG : s->variant;
+        const size_t smem = nc == 0 ? 0 : (A->d.dtype == RG_F32 ? cluster_smem_bytes<float>(A->d.side, rows, v)
+                                                                : cluster_smem_bytes<double>(A->d.side, rows, v));
+        S->use_small = real && A->d.kind == RG_CONST9 && block_T == 0 && nc > 0 &&
+                       s->precond != RG_PRECOND_JACOBI_FIELD && smem <= 200 * 1024;
+        S->cl_nc = nc;
+        S->cl_rows = rows;
+        S->cl_ppt = ppt;
     }
     S->kmax = (long long)max_outer * s->m;
     const dim3 g = step_grid(A);
@@ -782,30 +789,30 @@ int rg_solver_step(rg_solver* S, void* stream, int* steps_out) {
     if (S->use_small) {   // the whole solve (even max_outer = 0) in one launch
         const rg_op* A = S->A;
         cudaError_t err;
-        if (A->d.dtype == RG_F64) {
-            SmallArgs<double> a;
+        auto fill = [&](auto& a) {
             a.coef = (const double*)A->d.stencil;
             a.scale = S->s.precond == RG_PRECOND_JACOBI_SCALAR ? (const double*)S->s.scale : nullptr;
+            a.omega = S->s.omega; a.alpha = S->s.alpha; a.atil = S->s.alpha_tilde;
+            a.side = A->d.side; a.P = A->P; a.m = m; a.shared = A->d.shared; a.cfg = S->cfg;
+            a.nc = S->cl_nc; a.rows = S->cl_rows;
+            a.st = S->d_st; a.trace = S->d_trace; a.trace_stride = S->trace_stride;
+        };
+        const int var = S->s.variant >= RG_NAG ? V_NAG : S->s.variant;
+        const bool jac = S->s.precond == RG_PRECOND_JACOBI_SCALAR;
+        if (A->d.dtype == RG_F64) {
+            ClusterArgs<double> a;
+            fill(a);
             a.u = (double*)S->u[0];
             a.f = (const double*)S->f;
-            a.omega = S->s.omega; a.alpha = S->s.alpha; a.atil = S->s.alpha_tilde;
-            a.side = A->d.side; a.P = A->P; a.m = m; a.shared = A->d.shared; a.cfg = S->cfg;
-            a.st = S->d_st; a.trace = S->d_trace; a.trace_stride = S->trace_stride;
-            err = launch_small<double>(a, S->s.variant >= RG_NAG ? V_NAG : S->s.variant,
-                                       a.scale != nullptr, A->d.batch, st);
+            err = launch_cluster<double>(a, var, jac, S->cl_ppt, A->d.batch, st);
         } else {
-            SmallArgs<float> a;
-            a.coef = (const double*)A->d.stencil;
-            a.scale = S->s.precond == RG_PRECOND_JACOBI_SCALAR ? (const double*)S->s.scale : nullptr;
+            ClusterArgs<float> a;
+            fill(a);
             a.u = (float*)S->u[0];
             a.f = (const float*)S->f;
-            a.omega = S->s.omega; a.alpha = S->s.alpha; a.atil = S->s.alpha_tilde;
-            a.side = A->d.side; a.P = A->P; a.m = m; a.shared = A->d.shared; a.cfg = S->cfg;
-            a.st = S->d_st; a.trace = S->d_trace; a.trace_stride = S->trace_stride;
-            err = launch_small<float>(a, S->s.variant >= RG_NAG ? V_NAG : S->s.variant,
-                                      a.scale != nullptr, A->d.batch, st);
+            err = launch_cluster<float>(a, var, jac, S->cl_ppt, A->d.batch, st);
         }
-        if (err != cudaSuccess) return fail(RG_ECUDA, "small solve launch: %s", cudaGetErrorString(err));
+        if (err != cudaSuccess) return fail(RG_ECUDA, "cluster solve launch: %s", cudaGetErrorString(err));
         if (steps_out) *steps_out = (int)(S->kmax - S->k);
         S->k = S->kmax;
         S->small_done = true;

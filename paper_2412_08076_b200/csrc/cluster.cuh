@@ -1,0 +1,309 @@
+// cluster.cuh — the whole solve_stationary (richardson.py:77-141) in ONE
+// launch, one thread-block CLUSTER per system, for grids that fit in the
+// cluster's distributed shared memory (cfg1 63^2: 8 CTAs; cfg2 255^2: 16).
+//
+// CTA c of a cluster owns rows [c*R, c*R+R) of the system and keeps them,
+// plus one halo row above and below, in a zero-bordered shared-memory field
+// (u; for NAG also the look-ahead y, ping-ponged).  f, r, v of the CTA's own
+// points live in registers for the entire solve.  Per inner step:
+//
+//   update own points -> cluster.sync -> copy the two halo rows from the
+//   neighbouring CTAs' shared memory (DSMEM) -> residual of own points ->
+//   CTA partial of ||r||^2 written into every CTA's `parts` slot (DSMEM)
+//   -> cluster.sync -> every thread sums parts[0..nc) in the same order and
+//   takes the same convergence / divergence / max_outer decision.
+//
+// Nothing touches HBM between the initial load and the final store, and
+// there is no launch per step: the solve is bound by FP64 issue and the
+// two cluster barriers per step.  Arithmetic is the reference's (no FMA):
+// iterates are bitwise the oracle's.
+#pragma once
+#include <cooperative_groups.h>
+
+#include "reduce.cuh"
+
+namespace rg {
+namespace cg = cooperative_groups;
+
+constexpr int CL_NT = 256;
+constexpr int CL_MAXC = 16;     // non-portable cluster size limit
+
+template <typename S>
+struct ClusterArgs {
+    const CT<S>* coef;   // [B][9] (or one set when shared)
+    const CT<S>* scale;  // [B] Jacobi scale or null
+    S* u;                // [B][P] initial guess in, answer out
+    const S* f;          // [B][P]
+    const double* omega;
+    const double* alpha;
+    const double* atil;
+    int side, P, m;
+    int shared;
+    int nc;              // CTAs per cluster (= per system)
+    int rows;            // rows per CTA (the last CTA may own fewer)
+    SolveCfg cfg;
+    SysState* st;
+    double* trace;
+    int trace_stride;
+};
+
+template <typename S, int VAR, bool JAC, int PPT>
+__global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> a) {
+    typedef CT<S> C;
+    constexpr bool NAG = VAR >= V_NAG;
+    constexpr bool HASV = VAR != V_PLAIN;
+    cg::cluster_group cl = cg::this_cluster();
+    const int nc = a.nc;
+    const int crank = (int)cl.block_rank();
+    const int b = blockIdx.x / nc;
+    const int s = a.side, W = s + 2, m = a.m;
+    const int R = a.rows;
+    const int row0 = crank * R;
+    const int nrows = min(R, s - row0);          // >= 1 by construction
+    const int npts = nrows * s;
+    const int tid = threadIdx.x;
+    const size_t base = (size_t)b * a.P;
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* U = reinterpret_cast<C*>(smem_raw);                   // [(R+2) * W]
+    C* Yb[2] = {U + (R + 2) * W, U + 2 * (R + 2) * W};       // NAG ping-pong
+    __shared__ double parts[CL_MAXC];
+    __shared__ double red[CL_NT / 32];
+
+    C c[9];
+    const int cb = a.shared ? 0 : b;
+#pragma unroll
+    for (int d = 0; d < 9; ++d) c[d] = a.coef[(size_t)cb * 9 + d];
+    const C sc = JAC ? a.scale[b] : szero<C>();
+
+    const int fields = NAG ? 3 : 1;
+    for (int q = tid; q < fields * (R + 2) * W; q += CL_NT) U[q] = szero<C>();
+    __syncthreads();
+
+    C fr[PPT], rr[PPT], vr[PPT];
+    int pix[PPT];
+#pragma unroll
+    for (int j = 0; j < PPT; ++j) {
+        const int p = tid + j * CL_NT;
+        const int lr = p / s, col = p - (p / s) * s;
+        pix[j] = (lr + 1) * W + (col + 1);
+        const bool mine = p < npts;
+        const size_t g = base + (size_t)(row0 + lr) * s + col;
+        fr[j] = mine ? to_c(a.f[g]) : szero<C>();
+        vr[j] = szero<C>();                                    // v = 0 at entry (:95)
+        rr[j] = szero<C>();
+        if (mine) U[pix[j]] = to_c(a.u[g]);
+    }
+
+    // halo rows of field X from the neighbouring CTAs (DSMEM reads)
+    auto halo = [&](C* X) {
+        if (crank > 0) {
+            const C* up = cl.map_shared_rank(X, crank - 1);
+            for (int q = tid; q < s; q += CL_NT) X[q + 1] = up[R * W + q + 1];       // its last row
+        }
+        if (crank < nc - 1) {
+            const C* dn = cl.map_shared_rank(X, crank + 1);
+            for (int q = tid; q < s; q += CL_NT) X[(nrows + 1) * W + q + 1] = dn[W + q + 1];
+        }
+    };
+    auto stencil = [&](const C* X, int q) {                     // CSR order, no FMA
+        C t = mul(c[0], X[q - W - 1]);
+        t = add(t, mul(c[1], X[q - W]));
+        t = add(t, mul(c[2], X[q - W + 1]));
+        t = add(t, mul(c[3], X[q - 1]));
+        t = add(t, mul(c[4], X[q]));
+        t = add(t, mul(c[5], X[q + 1]));
+        t = add(t, mul(c[6], X[q + W - 1]));
+        t = add(t, mul(c[7], X[q + W]));
+        t = add(t, mul(c[8], X[q + W + 1]));
+        return t;
+    };
+    // cluster-wide sum, identical bits in every thread of every CTA
+    auto cluster_sum = [&](double v) {
+        const int lane = tid & 31, w = tid >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (lane == 0) red[w] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+#pragma unroll
+            for (int q = 0; q < CL_NT / 32; ++q) t += red[q];
+            for (int r = 0; r < nc; ++r) *cl.map_shared_rank(&parts[crank], r) = t;
+        }
+        cl.sync();
+        double tot = 0.0;
+        for (int r = 0; r < nc; ++r) tot += parts[r];
+        return tot;
+    };
+    auto residual_u = [&]() {
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+            if (tid + j * CL_NT < npts) {
+                rr[j] = sub(fr[j], stencil(U, pix[j]));
+                acc = sqacc(acc, rr[j]);
+            }
+        }
+        return acc;
+    };
+
+    const SolveCfg cf = a.cfg;
+    double* trace = a.trace + (size_t)b * a.trace_stride;
+    int status = ST_ACTIVE, outer = 0, inner = 0;
+    double fnorm, trace0, rel, bad_rel = 0.0;
+    cl.sync();                                                  // own rows loaded everywhere
+    halo(U);
+    __syncthreads();
+    {
+        double ff = 0.0;
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) ff = sqacc(ff, fr[j]);
+        const double r2 = cluster_sum(residual_u());
+        cl.sync();                                              // parts reused
+        const double f2 = cluster_sum(ff);
+        fnorm = sqrt(f2);
+        if (fnorm == 0.0) {                                     // :97-100
+            status = ST_CONVERGED; rel = 0.0; trace0 = 0.0;
+        } else {
+            rel = sqrt(r2) / fnorm;
+            trace0 = rel;
+            if (rel <= cf.tol) status = ST_CONVERGED;
+            else if (cf.max_outer <= 0) status = ST_MAXED;
+        }
+        if (tid == 0 && crank == 0) trace[0] = trace0;
+    }
+    const double div_thr = cf.div_factor * fmax(trace0, 1.0);
+    int k = 0;
+    while (status == ST_ACTIVE) {
+        const int i = k % m;
+        const double w = a.omega[b * m + i];
+        const double al = HASV ? a.alpha[b * m + i] : 0.0;
+        if (NAG) {
+            C* Y = Yb[k & 1];
+            const double at = a.atil[b * m + i];
+#pragma unroll
+            for (int j = 0; j < PPT; ++j)
+                if (tid + j * CL_NT < npts) Y[pix[j]] = add(U[pix[j]], rmul(at, vr[j]));   // (:119)
+            cl.sync();
+            halo(Y);
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < PPT; ++j)
+                if (tid + j * CL_NT < npts) rr[j] = sub(fr[j], stencil(Y, pix[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {                         // (:120-121)
+            if (tid + j * CL_NT < npts) {
+                const C p = JAC ? mul(sc, rr[j]) : rr[j];
+                C vn = (VAR == V_PLAIN) ? rmul(w, p) : add(rmul(al, vr[j]), rmul(w, p));
+                U[pix[j]] = stored<S>(add(U[pix[j]], vn));
+                vr[j] = stored<S>(vn);
+            }
+        }
+        ++k;
+        const bool test = !NAG || cf.check_inner || (k % m) == 0;   // (:123)
+        if (test) {
+            cl.sync();                                          // updates visible
+            halo(U);
+            __syncthreads();
+            const double r2 = cluster_sum(residual_u());
+            rel = sqrt(r2) / fnorm;
+            inner = k;
+            const bool boundary = (k % m) == 0;
+            if (!isfinite(rel) || rel > div_thr) {              // :126-129
+                status = ST_DIVERGED; bad_rel = rel;
+            } else {
+                if (boundary) {
+                    outer = k / m;
+                    if (tid == 0 && crank == 0) trace[outer] = rel;
+                }
+                if ((cf.check_inner || boundary) && rel <= cf.tol) {
+                    status = ST_CONVERGED;
+                    if (!boundary) { outer = k / m + 1; if (tid == 0 && crank == 0) trace[outer] = rel; }
+                } else if (boundary && outer >= cf.max_outer) {
+                    status = ST_MAXED;
+                }
+            }
+        }
+    }
+    if (tid == 0 && crank == 0) {
+        SysState& st = a.st[b];
+        st.fnorm = fnorm; st.trace0 = trace0; st.rel = rel; st.bad_rel = bad_rel;
+        st.status = status; st.outer = outer; st.inner = inner; st.ans_buf = 0; st.last_j = k;
+    }
+    if (status != ST_DIVERGED) {
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+            const int p = tid + j * CL_NT;
+            if (p < npts) {
+                const int lr = p / s, col = p - (p / s) * s;
+                a.u[base + (size_t)(row0 + lr) * s + col] = to_s<S>(U[pix[j]]);
+            }
+        }
+    }
+    cl.sync();   // no CTA may exit while others still read its shared memory
+}
+
+// Cluster shape for a side x side grid: nc CTAs (power of two <= 16), R rows
+// each, at most PPT * CL_NT points per CTA; nc = 0 if it does not fit.
+inline void cluster_shape(int side, int* nc, int* rows, int* ppt) {
+    const long long P = (long long)side * side;
+    int c = 1;
+    while (c < CL_MAXC && P > (long long)c * 512) c *= 2;      // ~2+ points per thread
+    while (c > 1 && (side + c - 1) / c < 2) c /= 2;             // >= 2 rows per CTA
+    const int R = (side + c - 1) / c;
+    if ((long long)R * side > 16LL * CL_NT || (c - 1) * R >= side) { *nc = 0; return; }
+    *nc = c;
+    *rows = R;
+    *ppt = (R * side + CL_NT - 1) / CL_NT <= 4 ? 4 : 16;
+}
+
+template <typename S>
+inline size_t cluster_smem_bytes(int side, int rows, int variant) {
+    return (size_t)(rows + 2) * (side + 2) * sizeof(CT<S>) * (variant >= V_NAG ? 3 : 1);
+}
+
+template <typename S, int VAR, bool JAC, int PPT>
+cudaError_t launch_cluster_k(const ClusterArgs<S>& a, int B, size_t smem, cudaStream_t st) {
+    auto kern = cluster_solve_kernel<S, VAR, JAC, PPT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (a.nc > 8) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(B * a.nc, 1, 1);
+    cfg.blockDim = dim3(CL_NT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <typename S>
+cudaError_t launch_cluster(const ClusterArgs<S>& a, int variant, bool jac, int ppt, int B,
+                           cudaStream_t st) {
+    const size_t smem = cluster_smem_bytes<S>(a.side, a.rows, variant);
+#define RG_CL(V, J, PP) return launch_cluster_k<S, V, J, PP>(a, B, smem, st)
+    if (ppt == 4) {
+        if (variant == V_PLAIN) { if (jac) RG_CL(V_PLAIN, true, 4); RG_CL(V_PLAIN, false, 4); }
+        if (variant == V_MOM) { if (jac) RG_CL(V_MOM, true, 4); RG_CL(V_MOM, false, 4); }
+        if (jac) RG_CL(V_NAG, true, 4);
+        RG_CL(V_NAG, false, 4);
+    }
+    if (variant == V_PLAIN) { if (jac) RG_CL(V_PLAIN, true, 16); RG_CL(V_PLAIN, false, 16); }
+    if (variant == V_MOM) { if (jac) RG_CL(V_MOM, true, 16); RG_CL(V_MOM, false, 16); }
+    if (jac) RG_CL(V_NAG, true, 16);
+    RG_CL(V_NAG, false, 16);
+#undef RG_CL
+}
+
+}  // namespace rg
