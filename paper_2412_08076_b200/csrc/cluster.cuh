@@ -1,6 +1,7 @@
 // cluster.cuh — the whole solve_stationary (richardson.py:77-141) in ONE
-// launch, one thread-block CLUSTER per system, for grids that fit in the
-// cluster's distributed shared memory (cfg1 63^2: 8 CTAs; cfg2 255^2: 16).
+// launch, one thread-block CLUSTER per system, for small grids (<= 4096
+// unknowns; cfg1 63^2 runs on 8 CTAs).  Larger grids (cfg2 255^2 measured
+// 160 ms here vs 86 ms tiled) go through the temporally blocked sweep.
 //
 // CTA c of a cluster owns rows [c*R, c*R+R) of the system and keeps them,
 // plus one halo row above and below, in a zero-bordered shared-memory field
@@ -10,8 +11,10 @@
 //   update own points -> cluster.sync -> copy the two halo rows from the
 //   neighbouring CTAs' shared memory (DSMEM) -> residual of own points ->
 //   CTA partial of ||r||^2 written into every CTA's `parts` slot (DSMEM)
-//   -> cluster.sync -> every thread sums parts[0..nc) in the same order and
-//   takes the same convergence / divergence / max_outer decision.
+//   -> every thread sums the partials in the same order and takes the same
+//   convergence / divergence / max_outer decision.
+// plain/mom pipeline the decision one step behind (one cluster barrier per
+// step, register backup of the previous iterate); nag uses two.
 //
 // Nothing touches HBM between the initial load and the final store, and
 // there is no launch per step: the solve is bound by FP64 issue and the
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
     for (int d = 0; d < 9; ++d) c[d] = a.coef[(size_t)cb * 9 + d];
     const C sc = JAC ? a.scale[b] : szero<C>();
 
-    const int fields = NAG ? 3 : 1;
+    const int fields = NAG ? 3 : 2;    // u (+ y ping-pong) | u ping-pong
     for (int q = tid; q < fields * (R + 2) * W; q += CL_NT) U[q] = szero<C>();
     __syncthreads();
 
@@ -136,17 +139,19 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
         for (int r = 0; r < nc; ++r) tot += parts[r];
         return tot;
     };
-    auto residual_u = [&]() {
+    auto residual_of = [&](const C* X) {
         double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < PPT; ++j) {
             if (tid + j * CL_NT < npts) {
-                rr[j] = sub(fr[j], stencil(U, pix[j]));
+                rr[j] = sub(fr[j], stencil(X, pix[j]));
                 acc = sqacc(acc, rr[j]);
             }
         }
         return acc;
     };
+    auto residual_u = [&]() { return residual_of(U); };
+    C* Uout = U;                          // field holding the answer at the end
 
     const SolveCfg cf = a.cfg;
     double* trace = a.trace + (size_t)b * a.trace_stride;
@@ -175,7 +180,85 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
     }
     const double div_thr = cf.div_factor * fmax(trace0, 1.0);
     int k = 0;
-    while (status == ST_ACTIVE) {
+    // decision for the residual of iterate j (richardson.py:124-136); identical
+    // in every thread because every thread sums the same partials in order
+    auto decide = [&](int j, double r2) {
+        rel = sqrt(r2) / fnorm;
+        inner = j;
+        const bool boundary = (j % m) == 0;
+        if (!isfinite(rel) || rel > div_thr) {                  // :126-129
+            status = ST_DIVERGED; bad_rel = rel;
+            return;
+        }
+        if (boundary) {
+            outer = j / m;
+            if (tid == 0 && crank == 0) trace[outer] = rel;
+        }
+        if ((cf.check_inner || boundary) && rel <= cf.tol) {
+            status = ST_CONVERGED;
+            if (!boundary) { outer = j / m + 1; if (tid == 0 && crank == 0) trace[outer] = rel; }
+        } else if (boundary && outer >= cf.max_outer) {
+            status = ST_MAXED;
+        }
+    };
+    if (!NAG && status == ST_ACTIVE) {
+        // plain / mom: ONE cluster barrier per inner step.  The u field is
+        // ping-ponged (iteration j reads Ub[j&1], writes Ub[(j+1)&1]), so a
+        // neighbour may start its next update while this CTA still copies
+        // halo rows.  Iteration j computes u_{j+1}, exchanges its halos,
+        // computes r_{j+1} and publishes its partial into parts2[(j+1)&1];
+        // it then decides for r_j from the partials published one iteration
+        // earlier.  A stop at j leaves the answer u_j in Ub[j&1].
+        __shared__ double parts2[2][CL_MAXC];
+        C* Ub[2] = {U, U + (R + 2) * W};
+        bool have_prev = false;           // partials of r_k available (k >= 1)
+        while (true) {
+            const int i = k % m;
+            const double w = a.omega[b * m + i];
+            const double al = HASV ? a.alpha[b * m + i] : 0.0;
+            const C* Uo = Ub[k & 1];
+            C* Un = Ub[(k + 1) & 1];
+#pragma unroll
+            for (int j = 0; j < PPT; ++j) {                     // (:120-121)
+                if (tid + j * CL_NT < npts) {
+                    const C p = JAC ? mul(sc, rr[j]) : rr[j];
+                    C vn = (VAR == V_PLAIN) ? rmul(w, p) : add(rmul(al, vr[j]), rmul(w, p));
+                    Un[pix[j]] = stored<S>(add(Uo[pix[j]], vn));
+                    vr[j] = stored<S>(vn);
+                }
+            }
+            cl.sync();
+            halo(Un);
+            __syncthreads();
+            {   // partial of r_{k+1} -> parts2[(k+1)&1] in every CTA
+                double v = residual_of(Un);
+                const int lane = tid & 31, wq = tid >> 5;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                if (lane == 0) red[wq] = v;
+                __syncthreads();
+                if (tid == 0) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int q = 0; q < CL_NT / 32; ++q) t += red[q];
+                    for (int r = 0; r < nc; ++r) *cl.map_shared_rank(&parts2[(k + 1) & 1][crank], r) = t;
+                }
+            }
+            if (have_prev) {              // decide for r_k (published last iteration)
+                double tot = 0.0;
+                for (int r = 0; r < nc; ++r) tot += parts2[k & 1][r];
+                decide(k, tot);
+                if (status != ST_ACTIVE) {
+                    Uout = Ub[k & 1];
+                    break;
+                }
+            }
+            have_prev = true;
+            ++k;
+        }
+        cl.sync();                        // last remote writes to parts2 complete
+    }
+    while (NAG && status == ST_ACTIVE) {
         const int i = k % m;
         const double w = a.omega[b * m + i];
         const double al = HASV ? a.alpha[b * m + i] : 0.0;
@@ -207,24 +290,7 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
             cl.sync();                                          // updates visible
             halo(U);
             __syncthreads();
-            const double r2 = cluster_sum(residual_u());
-            rel = sqrt(r2) / fnorm;
-            inner = k;
-            const bool boundary = (k % m) == 0;
-            if (!isfinite(rel) || rel > div_thr) {              // :126-129
-                status = ST_DIVERGED; bad_rel = rel;
-            } else {
-                if (boundary) {
-                    outer = k / m;
-                    if (tid == 0 && crank == 0) trace[outer] = rel;
-                }
-                if ((cf.check_inner || boundary) && rel <= cf.tol) {
-                    status = ST_CONVERGED;
-                    if (!boundary) { outer = k / m + 1; if (tid == 0 && crank == 0) trace[outer] = rel; }
-                } else if (boundary && outer >= cf.max_outer) {
-                    status = ST_MAXED;
-                }
-            }
+            decide(k, cluster_sum(residual_u()));
         }
     }
     if (tid == 0 && crank == 0) {
@@ -238,7 +304,7 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
             const int p = tid + j * CL_NT;
             if (p < npts) {
                 const int lr = p / s, col = p - (p / s) * s;
-                a.u[base + (size_t)(row0 + lr) * s + col] = to_s<S>(U[pix[j]]);
+                a.u[base + (size_t)(row0 + lr) * s + col] = to_s<S>(Uout[pix[j]]);
             }
         }
     }
@@ -250,6 +316,7 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
 inline void cluster_shape(int side, int* nc, int* rows, int* ppt) {
     const long long P = (long long)side * side;
     int c = 1;
+    if (P > 4096) { *nc = 0; return; }   // larger grids: the tiled blocked sweep is faster
     while (c < CL_MAXC && P > (long long)c * 512) c *= 2;      // ~2+ points per thread
     while (c > 1 && (side + c - 1) / c < 2) c /= 2;             // >= 2 rows per CTA
     const int R = (side + c - 1) / c;
@@ -261,7 +328,7 @@ inline void cluster_shape(int side, int* nc, int* rows, int* ppt) {
 
 template <typename S>
 inline size_t cluster_smem_bytes(int side, int rows, int variant) {
-    return (size_t)(rows + 2) * (side + 2) * sizeof(CT<S>) * (variant >= V_NAG ? 3 : 1);
+    return (size_t)(rows + 2) * (side + 2) * sizeof(CT<S>) * (variant >= V_NAG ? 3 : 2);
 }
 
 template <typename S, int VAR, bool JAC, int PPT>
