@@ -76,7 +76,10 @@ def run_cfg1():
     t0 = time.perf_counter()
     uo, ro = O.solve_stationary(A, f, s.omega, tol=1e-6)
     tcpu = time.perf_counter() - t0
+    upd = rep.inner_iterations * 63 * 63
     return {"config": "cfg1 Richardson(8) 63^2 f64 to 1e-6", "gpu_time_to_tol_s": float(np.median(times)),
+            "updates_per_s": upd / float(np.median(times)),
+            "note": "latency-bound: 1520 dependent inner steps of a 3969-point system on one 8-CTA cluster",
             "outer": rep.iterations, "inner": rep.inner_iterations,
             "cpu_time_to_tol_s": tcpu, "cpu_cores": 1,
             "parity": {"bitwise_u": bool(np.array_equal(u, uo)),
@@ -165,9 +168,12 @@ def run_cfg4():
     eng.u[0].zero_()
     eng.cur = 0
     u1 = eng.step(Fd).cpu().numpy()
+    alg = 4 * 1023 ** 2 * (24 * M + 32 + 16) * alts        # smoothing + correction + norm
     out = {"config": "cfg4 FNS 4 x 1023^2, M=8 + DST correction, 100 alternations",
            "gpu_time_100_alternations_s": t, "gpu_ms_per_alternation": 1e3 * t / alts,
-           "smoothing_updates_per_s": 4 * 1023 ** 2 * M * alts / t}
+           "smoothing_updates_per_s": 4 * 1023 ** 2 * M * alts / t,
+           "roofline": {"bound": "hbm", "algorithmic_bytes_per_alternation": alg / alts,
+                        "achieved_GBs": alg / t / 1e9, "frac": alg / t / 1e9 / HBM}}
     A0 = O.assemble_anisotropic(probs[0].epsilon, probs[0].theta, 1024)
     lam0 = lam[0].cpu().numpy()
     uo = O.fns_lite_step(A0, F[0], np.zeros(A0.shape[0]), np.full(8, 0.5), 8, lam0)
@@ -199,7 +205,14 @@ def run_cfg5():
     res = GG.fgmres_batched(op, Fd, precond_apply=lambda R: h.apply(R), cfg=cfg)
     torch.cuda.synchronize()
     tf = time.perf_counter() - t0
+    m = len(s.omega)
+    alg = 0.0
+    for k, lvl in enumerate(h.levels[:-1]):
+        per = 96 if k == 0 else 80 + 144
+        alg += len(F) * lvl.op.P * (2 * m * per + 64)    # pre+post smoothing + residual/transfers
     out = {"config": "cfg5 Helmholtz 4 x 1023^2 c128, V-cycle(NAG16, depth 7) in FGMRES(20) x5",
+           "roofline_vcycle": {"bound": "hbm", "algorithmic_bytes": alg, "achieved_GBs": alg / tv / 1e9,
+                               "frac": alg / tv / 1e9 / HBM},
            "depth": h.depth, "host_setup_s": t_setup, "gpu_ms_per_vcycle_batch4": 1e3 * tv,
            "fgmres_total_s": tf, "fgmres_iterations": [r.iterations for _, r in res],
            "fgmres_final_rel": [float(r.final_relative_residual) for _, r in res],
