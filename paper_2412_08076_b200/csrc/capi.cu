@@ -262,8 +262,7 @@ static int dst_pass(const rg_dst* D, int axis, int mode, const double* in, doubl
     a.lpc = D->lpc;
     a.mode = mode;
     a.scale = sqrt(2.0 / D->M);
-    const size_t smem = (size_t)D->lpc * (D->M * sizeof(double2) +
-                                          (mode == DST_TWICE_LAM ? D->side * sizeof(double) : 0));
+    const size_t smem = 2 * (size_t)D->lpc * D->M * sizeof(double2);   // Stockham ping-pong
     const dim3 grid((D->side + D->lpc - 1) / D->lpc, D->batch);
     if (axis == 0) {
         CUDA_TRY(cudaFuncSetAttribute(dst_lines_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -536,7 +535,7 @@ int rg_dst_create(rg_dst** out, int batch, int side) {
     D->M = M;
     D->logM = 0;
     while ((1 << D->logM) < M) ++D->logM;
-    int lpc = 4096 / M;
+    int lpc = 2048 / M;   // 2 x lpc x M x 16 B of shared memory per CTA
     D->lpc = lpc < 1 ? 1 : (lpc > 8 ? 8 : lpc);
     std::vector<double2> tw(M);
     for (int k = 0; k < M; ++k) {

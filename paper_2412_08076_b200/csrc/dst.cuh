@@ -5,8 +5,8 @@
 // its odd extension y of length 2M (y_j = x_j, y_{2M-j} = -x_j, y_0 = y_M = 0):
 //   Y_k = -2i sum_j x_j sin(pi j k / M)   =>   DST_k = -Im(Y_k) / 2.
 // The real length-2M FFT is computed as one complex length-M FFT of
-// z_j = y_{2j} + i y_{2j+1} (radix-2, in place in shared memory, loaded in
-// bit-reversed order), followed by the even/odd split
+// z_j = y_{2j} + i y_{2j+1} (Stockham radix-4, ping-pong in shared memory,
+// natural order), followed by the even/odd split
 //   Y_k = E_k + e^{-i pi k/M} O_k,  E_k = (Z_k + conj Z_{M-k})/2,
 //                                   O_k = (Z_k - conj Z_{M-k})/(2i).
 // Orthonormal scaling sqrt(2/M) per axis (scipy dstn type=1 norm="ortho").
@@ -35,65 +35,75 @@ struct DstArgs {
 };
 enum { DST_PLAIN = 0, DST_TWICE_LAM = 1, DST_ADD = 2 };
 
-__device__ __forceinline__ double2 cmul_conj_tw(double2 b, double2 c) {
-    // b * w with w = (c.x, -c.y) = exp(-i theta), c = (cos, sin)(theta)
-    return make_double2(fma(b.x, c.x, b.y * c.y), fma(b.y, c.x, -b.x * c.y));
+__device__ __forceinline__ double2 cmulf(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// exp(-i pi k / M) for 0 <= k < 2M from the table tw[k] = (cos, sin)(pi k / M), k < M
+__device__ __forceinline__ double2 tw_fwd(const double2* tw, int M, int k) {
+    const bool hi = k >= M;
+    const double2 c = __ldg(&tw[hi ? k - M : k]);
+    return hi ? make_double2(-c.x, c.y) : make_double2(c.x, -c.y);
 }
 
-// One complex radix-2 DIT FFT of length M on z (bit-reversed input order),
-// executed cooperatively by the CTA on `nl` lines stored back to back.
-// Stages are fused in pairs (radix-2^2): a thread loads the 4 elements
-// {i, i+h, i+2h, i+3h}, applies the two butterfly stages (half sizes h and
-// 2h) in registers and stores once -- half the shared-memory passes and
-// barriers of plain radix-2.  An odd log2(M) leaves one radix-2 stage.
-// Twiddle of stage half-size h at offset j: exp(-i pi j / h) = tw[j * M / h].
-__device__ inline void fft_lines(double2* z, int nl, int M, int logM, const double2* tw) {
-    int s = 1;
-    if (logM & 1) {                       // one radix-2 stage (h = 1, twiddle 1)
-        const int nb = nl * (M >> 1);
-        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
-            const int i0 = 2 * t;         // lines are contiguous, M even
-            const double2 a = z[i0], b = z[i0 + 1];
-            z[i0] = make_double2(a.x + b.x, a.y + b.y);
-            z[i0 + 1] = make_double2(a.x - b.x, a.y - b.y);
+// Complex forward FFT of length M (power of two) on nl lines stored back to
+// back, Stockham auto-sort (natural order in and out): one radix-2 pass when
+// log2(M) is odd, then radix-4 passes.  Pass with sub-transform length Ns:
+// thread j reads the 4 values at stride M/4 (contiguous across lanes),
+// twiddles them by exp(-2 pi i (j mod Ns) r / 4Ns), does the 4-point DFT and
+// writes them at idx = (j / Ns) 4 Ns + (j mod Ns) + r Ns.  Ping-pongs between
+// A and B; returns the buffer holding the result.
+__device__ inline double2* fft_lines(double2* A, double2* B, int nl, int M, int logM,
+                                     const double2* tw) {
+    double2* in = A;
+    double2* out = B;
+    int Ns = 1;
+    if (logM & 1) {
+        const int h = M >> 1;
+        for (int t = threadIdx.x; t < nl * h; t += blockDim.x) {
+            const int line = t / h, j = t - line * h;
+            const double2 a = in[line * M + j], b = in[line * M + j + h];
+            out[line * M + 2 * j] = make_double2(a.x + b.x, a.y + b.y);
+            out[line * M + 2 * j + 1] = make_double2(a.x - b.x, a.y - b.y);
         }
         __syncthreads();
-        s = 2;
+        double2* tmp = in; in = out; out = tmp;
+        Ns = 2;
     }
-    for (; s < logM; s += 2) {
-        const int h = 1 << (s - 1);       // first stage half-size; second is 2h
-        const int nq = nl * (M >> 2);     // 4-element groups over all lines
-        for (int t = threadIdx.x; t < nq; t += blockDim.x) {
-            const int line = t / (M >> 2);
-            const int g = t - line * (M >> 2);
-            const int blk = g / h, j = g - blk * h;
-            const int i0 = line * M + blk * 4 * h + j;
-            double2 x0 = z[i0], x1 = z[i0 + h], x2 = z[i0 + 2 * h], x3 = z[i0 + 3 * h];
-            // stage s: pairs (x0,x1), (x2,x3) with exp(-i pi j / h)
-            const double2 w1 = __ldg(&tw[j * (M / h)]);
-            double2 p = cmul_conj_tw(x1, w1);
-            double2 q = cmul_conj_tw(x3, w1);
-            double2 a0 = make_double2(x0.x + p.x, x0.y + p.y), a1 = make_double2(x0.x - p.x, x0.y - p.y);
-            double2 a2 = make_double2(x2.x + q.x, x2.y + q.y), a3 = make_double2(x2.x - q.x, x2.y - q.y);
-            // stage s+1: pairs (a0,a2) with exp(-i pi j / 2h), (a1,a3) with exp(-i pi (j+h) / 2h)
-            const double2 w2 = __ldg(&tw[j * (M / (2 * h))]);
-            const double2 w3 = __ldg(&tw[(j + h) * (M / (2 * h))]);
-            p = cmul_conj_tw(a2, w2);
-            q = cmul_conj_tw(a3, w3);
-            z[i0] = make_double2(a0.x + p.x, a0.y + p.y);
-            z[i0 + 2 * h] = make_double2(a0.x - p.x, a0.y - p.y);
-            z[i0 + h] = make_double2(a1.x + q.x, a1.y + q.y);
-            z[i0 + 3 * h] = make_double2(a1.x - q.x, a1.y - q.y);
+    const int q = M >> 2;
+    for (; Ns < M; Ns <<= 2) {
+        const int kstep = M / (2 * Ns);          // twiddle index step per (jm * r)
+        for (int t = threadIdx.x; t < nl * q; t += blockDim.x) {
+            const int line = t / q, j = t - line * q;
+            const double2* x = in + line * M + j;
+            double2 v0 = x[0], v1 = x[q], v2 = x[2 * q], v3 = x[3 * q];
+            const int jm = j & (Ns - 1);
+            if (jm) {
+                v1 = cmulf(v1, tw_fwd(tw, M, jm * kstep));
+                v2 = cmulf(v2, tw_fwd(tw, M, 2 * jm * kstep));
+                v3 = cmulf(v3, tw_fwd(tw, M, 3 * jm * kstep));
+            }
+            const double2 a = make_double2(v0.x + v2.x, v0.y + v2.y);
+            const double2 b = make_double2(v0.x - v2.x, v0.y - v2.y);
+            const double2 c = make_double2(v1.x + v3.x, v1.y + v3.y);
+            const double2 d = make_double2(v1.x - v3.x, v1.y - v3.y);
+            double2* y = out + line * M + (j - jm) * 4 + jm;
+            y[0] = make_double2(a.x + c.x, a.y + c.y);
+            y[Ns] = make_double2(b.x + d.y, b.y - d.x);          // b - i d
+            y[2 * Ns] = make_double2(a.x - c.x, a.y - c.y);
+            y[3 * Ns] = make_double2(b.x - d.y, b.y + d.x);      // b + i d
         }
         __syncthreads();
+        double2* tmp = in; in = out; out = tmp;
     }
+    return in;
 }
 
-// Load nl lines (line l reads x(l, j) for j = 1..N via `get`) as packed z in
-// bit-reversed order.  LINES_FAST: consecutive threads take consecutive
-// lines (strided column lines -> coalesced row segments).
+// Load nl lines (line l reads x(l, j) for j = 1..N via `get`) as packed
+// z_j = y_2j + i y_2j+1 of the odd extension, natural order.  LINES_FAST:
+// consecutive threads take consecutive lines (strided column lines ->
+// coalesced row segments).
 template <bool LINES_FAST, class Get>
-__device__ inline void load_lines(double2* z, int nl, int M, int logM, Get get) {
+__device__ inline void load_lines(double2* z, int nl, int M, Get get) {
     const int N = M - 1;
     for (int t = threadIdx.x; t < nl * M; t += blockDim.x) {
         const int l = LINES_FAST ? t % nl : t / M;
@@ -108,8 +118,7 @@ __device__ inline void load_lines(double2* z, int nl, int M, int logM, Get get) 
             ye = (me <= N) ? -get(l, me) : 0.0;
             yo = (mo >= 1 && mo <= N) ? -get(l, mo) : 0.0;
         }
-        const int r = __brev(j) >> (32 - logM);
-        z[l * M + r] = make_double2(ye, yo);
+        z[l * M + j] = make_double2(ye, yo);
     }
     __syncthreads();
 }
@@ -131,9 +140,9 @@ __device__ inline double dst_coeff(const double2* z, int l, int M, int k, const 
 template <int AXIS>
 __global__ void __launch_bounds__(DST_NT) dst_lines_kernel(DstArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2* z = reinterpret_cast<double2*>(smem_raw);
-    double* stage = reinterpret_cast<double*>(z + a.lpc * a.M);   // [lpc][N] (TWICE_LAM)
     const int N = a.N, M = a.M;
+    double2* zA = reinterpret_cast<double2*>(smem_raw);
+    double2* zB = zA + a.lpc * M;
     const size_t NN = (size_t)N * N;
     const int b = blockIdx.y;                           // system
     const int l0 = blockIdx.x * a.lpc;                  // first line of this CTA
@@ -142,11 +151,12 @@ __global__ void __launch_bounds__(DST_NT) dst_lines_kernel(DstArgs a) {
     auto addr = [&](int l, int j) -> size_t {           // element j (1-based) of line l0+l
         return AXIS == 0 ? (size_t)(l0 + l) * N + (j - 1) : (size_t)(j - 1) * N + (l0 + l);
     };
-    load_lines<AXIS == 1>(z, nl, M, a.logM, [&](int l, int j) { return in[addr(l, j)]; });
-    fft_lines(z, nl, M, a.logM, a.tw);
+    load_lines<AXIS == 1>(zA, nl, M, [&](int l, int j) { return in[addr(l, j)]; });
+    double2* z = fft_lines(zA, zB, nl, M, a.logM, a.tw);
     double* out = a.out + b * NN;
     if (a.mode == DST_TWICE_LAM) {
         const double* lam = a.lam + b * NN;
+        double* stage = reinterpret_cast<double*>(z == zA ? zB : zA);   // the free buffer
         for (int t = threadIdx.x; t < nl * N; t += blockDim.x) {
             // column layout: consecutive threads walk lines first (coalesced segments)
             const int l = AXIS == 1 ? t % nl : t / N;
@@ -154,8 +164,9 @@ __global__ void __launch_bounds__(DST_NT) dst_lines_kernel(DstArgs a) {
             stage[l * N + (k - 1)] = a.scale * dst_coeff(z, l, M, k, a.tw) * lam[addr(l, k)];
         }
         __syncthreads();
-        load_lines<false>(z, nl, M, a.logM, [&](int l, int j) { return stage[l * N + (j - 1)]; });
-        fft_lines(z, nl, M, a.logM, a.tw);
+        double2* dst = z;                                   // reload into the FFT buffer
+        load_lines<false>(dst, nl, M, [&](int l, int j) { return stage[l * N + (j - 1)]; });
+        z = fft_lines(dst, dst == zA ? zB : zA, nl, M, a.logM, a.tw);
     }
     for (int t = threadIdx.x; t < nl * N; t += blockDim.x) {
         const int l = AXIS == 1 ? t % nl : t / N;
