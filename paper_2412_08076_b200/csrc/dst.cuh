@@ -60,7 +60,7 @@ __device__ inline double2* fft_lines(double2* A, double2* B, int nl, int M, int 
     if (logM & 1) {
         const int h = M >> 1;
         for (int t = threadIdx.x; t < nl * h; t += blockDim.x) {
-            const int line = t / h, j = t - line * h;
+            const int line = t >> (logM - 1), j = t & (h - 1);
             const double2 a = in[line * M + j], b = in[line * M + j + h];
             out[line * M + 2 * j] = make_double2(a.x + b.x, a.y + b.y);
             out[line * M + 2 * j + 1] = make_double2(a.x - b.x, a.y - b.y);
@@ -73,7 +73,7 @@ __device__ inline double2* fft_lines(double2* A, double2* B, int nl, int M, int 
     for (; Ns < M; Ns <<= 2) {
         const int kstep = M / (2 * Ns);          // twiddle index step per (jm * r)
         for (int t = threadIdx.x; t < nl * q; t += blockDim.x) {
-            const int line = t / q, j = t - line * q;
+            const int line = t >> (logM - 2), j = t & (q - 1);
             const double2* x = in + line * M + j;
             double2 v0 = x[0], v1 = x[q], v2 = x[2 * q], v3 = x[3 * q];
             const int jm = j & (Ns - 1);
@@ -105,9 +105,10 @@ __device__ inline double2* fft_lines(double2* A, double2* B, int nl, int M, int 
 template <bool LINES_FAST, class Get>
 __device__ inline void load_lines(double2* z, int nl, int M, Get get) {
     const int N = M - 1;
+    const int logM = __ffs(M) - 1;
     for (int t = threadIdx.x; t < nl * M; t += blockDim.x) {
-        const int l = LINES_FAST ? t % nl : t / M;
-        const int j = LINES_FAST ? t / nl : t - l * M;
+        const int l = LINES_FAST ? t % nl : t >> logM;
+        const int j = LINES_FAST ? t / nl : t & (M - 1);
         double ye, yo;   // y_{2j}, y_{2j+1}
         const int e = 2 * j, o = 2 * j + 1;
         if (e < M) {
