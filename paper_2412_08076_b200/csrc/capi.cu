@@ -262,31 +262,6 @@ static int dst_pass(const rg_dst* D, int axis, int mode, const double* in, doubl
     a.lpc = D->lpc;
     a.mode = mode;
     a.scale = sqrt(2.0 / D->M);
-    if (D->M >= 32 && D->M <= 1024) {   // register-resident 4-step FFT, one warp per line
-        const int R2 = D->M / 32;
-        const size_t smem4 = (size_t)DST4_NW * R2 * 33 * sizeof(double2) +
-                             (mode == DST_TWICE_LAM ? (size_t)DST4_NW * D->side * sizeof(double) : 0);
-        const dim3 grid4((D->side + DST4_NW - 1) / DST4_NW, D->batch);
-#define RG_DST4(AX, R)                                                                              \
-    do {                                                                                            \
-        CUDA_TRY(cudaFuncSetAttribute(dst4_lines_kernel<AX, R>,                                     \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem4));    \
-        dst4_lines_kernel<AX, R><<<grid4, DST4_NW * 32, smem4, st>>>(a);                            \
-    } while (0)
-#define RG_DST4_AX(R) do { if (axis == 0) RG_DST4(0, R); else RG_DST4(1, R); } while (0)
-        switch (R2) {
-            case 1: RG_DST4_AX(1); break;
-            case 2: RG_DST4_AX(2); break;
-            case 4: RG_DST4_AX(4); break;
-            case 8: RG_DST4_AX(8); break;
-            case 16: RG_DST4_AX(16); break;
-            default: RG_DST4_AX(32); break;
-        }
-#undef RG_DST4_AX
-#undef RG_DST4
-        LAUNCH_CHECK();
-        return RG_OK;
-    }
     const size_t smem = 2 * (size_t)D->lpc * D->M * sizeof(double2);   // Stockham ping-pong
     const dim3 grid((D->side + D->lpc - 1) / D->lpc, D->batch);
     if (axis == 0) {
@@ -568,11 +543,8 @@ int rg_dst_create(rg_dst** out, int batch, int side) {
         const double ang = M_PI * (double)k / (double)M;
         tw[k] = make_double2(cos(ang), sin(ang));
     }
-    double2 tw32[16];
-    for (int j = 0; j < 16; ++j) tw32[j] = make_double2(cos(M_PI * j / 16.0), sin(M_PI * j / 16.0));
     cudaError_t e;
-    if ((e = cudaMemcpyToSymbol(c_tw32, tw32, sizeof tw32)) != cudaSuccess ||
-        (e = cudaMalloc((void**)&D->tw, sizeof(double2) * M)) != cudaSuccess ||
+    if ((e = cudaMalloc((void**)&D->tw, sizeof(double2) * M)) != cudaSuccess ||
         (e = cudaMalloc((void**)&D->work, sizeof(double) * (size_t)batch * side * side)) != cudaSuccess ||
         (e = cudaMemcpy(D->tw, tw.data(), sizeof(double2) * M, cudaMemcpyHostToDevice)) != cudaSuccess) {
         cudaFree(D->tw);

@@ -137,143 +137,6 @@ __device__ inline double dst_coeff(const double2* z, int l, int M, int k, const 
     return -0.5 * im;
 }
 
-// ---- register-resident "4-step" FFT for 32 <= M <= 1024 (M = 32 * R2) ----
-// One warp per line.  Step 1: lane n1 holds x[n1 + 32 n2] (n2 < R2) and does
-// an R2-point FFT in registers; twiddle by exp(-2 pi i n1 k2 / M); write to a
-// padded transpose T[k2 * 33 + n1] (conflict-free).  Step 2: lane k2 (< R2)
-// reads T[k2 * 33 + n1] (n1 < 32), does a 32-point FFT in registers and
-// produces X[k2 + R2 k1].  Only __syncwarp inside a line; in-register
-// twiddles exp(-i pi j / 16) come from constant memory (compile-time index).
-__constant__ double2 c_tw32[16];   // (cos, sin)(pi j / 16), filled by rg_dst_create
-
-template <int R>
-__device__ __forceinline__ void fft_reg(double2 (&v)[R]) {
-    constexpr int LOG = (R >= 32) ? 5 : (R >= 16) ? 4 : (R >= 8) ? 3 : (R >= 4) ? 2 : (R >= 2) ? 1 : 0;
-#pragma unroll
-    for (int i = 0; i < R; ++i) {                 // compile-time bit reversal
-        int j = 0;
-#pragma unroll
-        for (int b = 0; b < LOG; ++b) j |= ((i >> b) & 1) << (LOG - 1 - b);
-        if (j > i) { const double2 t = v[i]; v[i] = v[j]; v[j] = t; }
-    }
-#pragma unroll
-    for (int h = 1; h < R; h <<= 1) {
-#pragma unroll
-        for (int g = 0; g < R; g += 2 * h) {
-#pragma unroll
-            for (int j = 0; j < h; ++j) {
-                const double2 a = v[g + j];
-                double2 b = v[g + j + h];
-                if (j != 0) {                     // exp(-i pi j / h) = c_tw32[j * 16 / h] conj
-                    const double2 c = c_tw32[j * (16 / h)];
-                    b = make_double2(fma(b.x, c.x, b.y * c.y), fma(b.y, c.x, -b.x * c.y));
-                }
-                v[g + j] = make_double2(a.x + b.x, a.y + b.y);
-                v[g + j + h] = make_double2(a.x - b.x, a.y - b.y);
-            }
-        }
-    }
-}
-
-// FFT of the line stored at zl (natural order, M = 32 * R2 entries, buffer of
-// R2 * 33 entries); result back in zl, natural order.  Called by one warp.
-template <int R2>
-__device__ __forceinline__ void fft_line_warp(double2* zl, int M, const double2* tw) {
-    const int lane = threadIdx.x & 31;
-    double2 v[R2];
-#pragma unroll
-    for (int n2 = 0; n2 < R2; ++n2) v[n2] = zl[lane + 32 * n2];
-    fft_reg<R2>(v);
-#pragma unroll
-    for (int k2 = 1; k2 < R2; ++k2) {
-        if (lane) v[k2] = cmulf(v[k2], tw_fwd(tw, M, 2 * lane * k2));   // exp(-2 pi i n1 k2 / M)
-    }
-    __syncwarp();
-#pragma unroll
-    for (int k2 = 0; k2 < R2; ++k2) zl[k2 * 33 + lane] = v[k2];
-    __syncwarp();
-    if (lane < R2) {
-        double2 w[32];
-#pragma unroll
-        for (int n1 = 0; n1 < 32; ++n1) w[n1] = zl[lane * 33 + n1];
-        fft_reg<32>(w);
-        __syncwarp((R2 >= 32) ? 0xffffffffu : ((1u << R2) - 1u));   // all reads of T done
-#pragma unroll
-        for (int k1 = 0; k1 < 32; ++k1) zl[lane + R2 * k1] = w[k1];
-    }
-    __syncwarp();
-}
-
-constexpr int DST4_NW = 4;   // warps (= lines) per CTA
-
-template <int AXIS, int R2>
-__global__ void __launch_bounds__(DST4_NW * 32) dst4_lines_kernel(DstArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int N = a.N, M = a.M;
-    constexpr int LB = R2 * 33;                     // complex entries per line buffer
-    double2* z = reinterpret_cast<double2*>(smem_raw);
-    double* stage = reinterpret_cast<double*>(z + DST4_NW * LB);   // [NW][N] (TWICE_LAM)
-    const size_t NN = (size_t)N * N;
-    const int b = blockIdx.y;
-    const int l0 = blockIdx.x * DST4_NW;
-    const int nl = min(DST4_NW, N - l0);
-    const int wp = threadIdx.x >> 5;
-    const double* in = a.in + b * NN;
-    auto addr = [&](int l, int j) -> size_t {
-        return AXIS == 0 ? (size_t)(l0 + l) * N + (j - 1) : (size_t)(j - 1) * N + (l0 + l);
-    };
-    // packed odd extension, line l at z + l * LB
-    auto load = [&](auto get) {
-        for (int t = threadIdx.x; t < nl * M; t += blockDim.x) {
-            const int l = AXIS == 1 ? t % nl : t / M;
-            const int j = AXIS == 1 ? t / nl : t - (t / M) * M;
-            double ye, yo;
-            const int e = 2 * j, o = 2 * j + 1;
-            if (e < M) {
-                ye = (e >= 1) ? get(l, e) : 0.0;
-                yo = (o <= N) ? get(l, o) : 0.0;
-            } else {
-                const int me = 2 * M - e, mo = 2 * M - o;
-                ye = (me <= N) ? -get(l, me) : 0.0;
-                yo = (mo >= 1 && mo <= N) ? -get(l, mo) : 0.0;
-            }
-            z[l * LB + j] = make_double2(ye, yo);
-        }
-        __syncthreads();
-        if (wp < nl) fft_line_warp<R2>(z + wp * LB, M, a.tw);
-        __syncthreads();
-    };
-    auto coeff = [&](int l, int k) {                 // unscaled DST_k of line l
-        const double2 zk = z[l * LB + k];
-        const double2 zm = z[l * LB + (M - k)];
-        const double ex_im = 0.5 * (zk.y - zm.y);
-        const double dre = zk.x - zm.x, dim = zk.y + zm.y;
-        const double ore = 0.5 * dim, oim = -0.5 * dre;
-        const double2 w = __ldg(&a.tw[k]);
-        return -0.5 * (ex_im + (w.x * oim - w.y * ore));
-    };
-    load([&](int l, int j) { return in[addr(l, j)]; });
-    double* out = a.out + b * NN;
-    if (a.mode == DST_TWICE_LAM) {
-        const double* lam = a.lam + b * NN;
-        for (int t = threadIdx.x; t < nl * N; t += blockDim.x) {
-            const int l = AXIS == 1 ? t % nl : t / N;
-            const int k = AXIS == 1 ? t / nl + 1 : t - (t / N) * N + 1;
-            stage[l * N + (k - 1)] = a.scale * coeff(l, k) * lam[addr(l, k)];
-        }
-        __syncthreads();
-        load([&](int l, int j) { return stage[l * N + (j - 1)]; });
-    }
-    for (int t = threadIdx.x; t < nl * N; t += blockDim.x) {
-        const int l = AXIS == 1 ? t % nl : t / N;
-        const int k = AXIS == 1 ? t / nl + 1 : t - (t / N) * N + 1;
-        const double v = a.scale * coeff(l, k);
-        const size_t q = addr(l, k);
-        if (a.mode == DST_ADD) out[q] = out[q] + v;
-        else out[q] = v;
-    }
-}
-
 // Row (AXIS=0) or column (AXIS=1) pass over all B*N lines.
 template <int AXIS>
 __global__ void __launch_bounds__(DST_NT) dst_lines_kernel(DstArgs a) {
