@@ -261,3 +261,48 @@ def test_f32_cfg2_hard_system_within_1e5():
     uo, ro = O.solve_stationary(A, f, s.omega, s.alpha, variant="nag", tol=1e-300, max_outer=200)
     assert np.linalg.norm(u32 - uo) <= 1e-5 * np.linalg.norm(uo)
     assert np.all(np.abs(rep.trace - ro["trace"]) <= 1e-5 * ro["trace"])
+
+
+def test_spectral_bounds_vs_oracle_recipe(golden):
+    """GPU power iterations (spectral.py drop-in): the cfg1 50-step recipe and
+    the converged estimators agree with the reference's numbers."""
+    from paper_2412_08076_b200 import spectral as GS
+    d = golden("cfg1")
+    A = O.assemble_anisotropic(float(d["eps"]), float(d["theta"]), int(d["n"]))
+    lmax, _ = GS.power_iterations(A, 50, seed=0)
+    assert abs(lmax - float(d["lmax50"])) <= 1e-12 * abs(float(d["lmax50"]))
+    sig = 1.01 * lmax
+    ls, _ = GS.power_iterations(A, 50, seed=0, shift=sig)
+    assert abs((sig - ls) - float(d["lmin50"])) <= 1e-10 * float(d["lmin50"])
+    b = GS.estimate_lambda_max(A, tol=1e-10)
+    lam = np.linalg.eigvalsh(A.toarray())
+    assert abs(b.lambda_max - lam[-1]) <= 1e-6 * lam[-1]
+    with pytest.raises(GS.PowerIterationError):
+        GS.estimate_lambda_min(A, b.lambda_max, tol=1e-14, max_iter=20)
+
+
+def test_cfg2_full_system_bitwise():
+    """One full cfg2 system at BASELINE size (255^2, NAG(16), 200 sweeps,
+    MLP weights) on the GPU equals the oracle bit for bit."""
+    from paper_2412_08076_b200 import configs as CF
+    c = CF.cfg2(batch=2)
+    p, s, f = c["problems"][1], c["schedules"][1], c["F"][1]
+    A = O.assemble_anisotropic(p.epsilon, p.theta, 256)
+    u, rep = G.solve_stationary(A, f, s, tol=1e-300, max_outer=200)
+    uo, ro = O.solve_stationary(A, f, s.omega, s.alpha, variant="nag", tol=1e-300, max_outer=200)
+    assert rep.inner_iterations == ro["inner_iterations"] == 3200
+    assert np.array_equal(u, uo)
+    _close_trace(rep.trace, ro["trace"])
+
+
+def test_table2_known_answer_counts(golden):
+    """Acceptance criterion 1 analogue (test_acceptance.py:42-66): Chebyshev
+    m=3, N=64, theta=0, seed 0 -- the GPU reproduces the reference's
+    iteration counts exactly."""
+    d = golden("table2")
+    for k in range(2):
+        A = O.assemble_anisotropic(float(d[f"e{k}_eps"]), 0.0, 64)
+        f = np.random.default_rng(0).standard_normal(A.shape[0])
+        _, rep = G.solve_stationary(A, f, G.WeightSchedule(omega=d[f"e{k}_omega"]))
+        assert rep.iterations == d[f"e{k}_iterations"]
+        assert rep.inner_iterations == d[f"e{k}_inner"]
