@@ -89,7 +89,8 @@ static size_t scalar_bytes(int dtype) {
 
 static dim3 step_grid(const rg_op* A) {
     const int side = A->d.side;
-    return dim3((side + STEP_BX - 1) / STEP_BX, (side + STEP_BY - 1) / STEP_BY, A->d.batch);
+    return dim3((side + STEP_BX - 1) / STEP_BX, (side + STEP_BY * STEP_RPT - 1) / (STEP_BY * STEP_RPT),
+                A->d.batch);
 }
 
 template <typename S>
@@ -384,7 +385,8 @@ int rg_matvec(const rg_op* A, const void* x, void* y, void* stream) {
     if (rc) return rc;
     if (!x || !y) return fail(RG_ENULL, "null vector");
     cudaStream_t st = (cudaStream_t)stream;
-    const dim3 g = step_grid(A), blk(STEP_BX, STEP_BY);
+    const dim3 g((A->d.side + STEP_BX - 1) / STEP_BX, (A->d.side + STEP_BY - 1) / STEP_BY, A->d.batch);
+    const dim3 blk(STEP_BX, STEP_BY);
 #define MV(S, K) matvec_kernel<S, K><<<g, blk, 0, st>>>(view<S>(A), (const S*)x, (S*)y)
     switch (A->d.dtype * 10 + A->d.kind) {
         case RG_F32 * 10 + RG_CONST9: MV(float, K_CONST9); break;

@@ -92,6 +92,9 @@ struct StepArgs {
 };
 
 constexpr int STEP_BX = 32, STEP_BY = 8, STEP_NT = STEP_BX * STEP_BY;
+// rows per thread of step1_kernel (rows i, i + STEP_BY, ...): more loads in
+// flight per thread for the HBM-bound one-step sweeps
+constexpr int STEP_RPT = 2;
 
 template <typename S, int KIND>
 __global__ void __launch_bounds__(STEP_NT) step1_kernel(StepArgs<S> a) {
@@ -102,19 +105,19 @@ __global__ void __launch_bounds__(STEP_NT) step1_kernel(StepArgs<S> a) {
     if (a.use_status && a.epi.st[b].status != ST_ACTIVE) return;  // uniform per CTA
 
     const int j = blockIdx.x * STEP_BX + threadIdx.x;
-    const int i = blockIdx.y * STEP_BY + threadIdx.y;
-    const bool in = (i < side) && (j < side);
     const size_t base = (size_t)b * a.A.P;
-    const size_t idx = (size_t)i * side + j;
     const bool nag = a.variant >= V_NAG;
     const int si = b * a.m + a.i;
-
     typedef CT<S> C;
     double acc[1] = {0.0};
     double facc = 0.0;
-    if (in) {
-        const S* u = a.u_in + base;
-        const S* v = a.v_in ? a.v_in + base : nullptr;
+    const S* u = a.u_in + base;
+    const S* v = a.v_in ? a.v_in + base : nullptr;
+#pragma unroll
+    for (int rr = 0; rr < STEP_RPT; ++rr) {
+        const int i = (blockIdx.y * STEP_RPT + rr) * STEP_BY + threadIdx.y;
+        if (i >= side || j >= side) continue;
+        const size_t idx = (size_t)i * side + j;
         auto Xu = [&](int di, int dj) -> C {
             const int ii = i + di, jj = j + dj;
             if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
