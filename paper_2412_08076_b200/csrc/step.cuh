@@ -92,9 +92,9 @@ struct StepArgs {
 };
 
 constexpr int STEP_BX = 32, STEP_BY = 8, STEP_NT = STEP_BX * STEP_BY;
-// rows per thread of step1_kernel (rows i, i + STEP_BY, ...): more loads in
-// flight per thread for the HBM-bound one-step sweeps
-constexpr int STEP_RPT = 2;
+// rows per thread of step1_kernel (rows i, i + STEP_BY, ...); 2 measured
+// slower than 1 on the complex V-cycle smoother (5.87 vs 5.45 ms per cycle)
+constexpr int STEP_RPT = 1;
 
 template <typename S, int KIND>
 __global__ void __launch_bounds__(STEP_NT) step1_kernel(StepArgs<S> a) {
