@@ -131,3 +131,31 @@ def test_symbol_bounds_match_dense_spectrum():
     lam = np.linalg.eigvalsh(O.assemble_anisotropic(0.1, 0.5, 24).toarray())
     assert lmax >= lam[-1] * (1 - 1e-3) and lmax <= lam[-1] * 1.05
     assert lam[0] / 8 <= lmin <= lam[0] * 1.001
+
+
+@pytest.mark.reference
+def test_reference_objects_are_accepted(richlab):
+    """The drop-in consumes richlab's own objects: SparseMatrix (CSR arrays),
+    Preconditioner.weighted_jacobi (scale recovered exactly through apply),
+    WeightSchedule (duck-typed)."""
+    from paper_2412_08076_b200.operator import precond_scale
+    from paper_2412_08076_b200.richardson import _sched_list
+    R = richlab
+    p = R.AnisotropicProblem(0.01, 0.8, 24)
+    A = R.assemble_anisotropic(p)
+    s1, pl1, pr1 = extract_planes(A)
+    s2, pl2, pr2 = extract_planes(A.to_scipy())
+    assert s1 == s2 == 23 and np.array_equal(pl1, pl2) and np.array_equal(pr1, pr2)
+    kind, c = classify(s1, pl1, pr1)
+    assert kind == "const9" and np.array_equal(c, anisotropic_stencil(AnisotropicProblem(0.01, 0.8, 24)))
+    P = R.Preconditioner.weighted_jacobi(A)
+    sc = precond_scale(P, A.ncols)
+    assert sc.ndim == 0 and sc == (2.0 / 3.0) / A.diagonal()[0]
+    with pytest.raises(UnsupportedOperator):
+        precond_scale(R.Preconditioner.ssor(A), A.ncols)
+    ws = R.WeightSchedule(omega=[0.1, 0.2], alpha=[0.3, 0.4], variant="nag")
+    (s,) = _sched_list(ws, 1)
+    assert np.array_equal(s.alpha_tilde, [0.3, 0.4]) and s.m == 2
+    H = R.assemble_helmholtz(R.HelmholtzProblem(2 * np.pi * 64 / 10, 64))
+    kind, (off, diag) = classify(*extract_planes(H))
+    assert kind == "diag5" and np.array_equal(diag, H.diagonal())
