@@ -40,13 +40,11 @@ class FgmresConfig:
 
 
 class _Sys:
-    """Per-system FGMRES state (the locals of fgmres.py:31-131)."""
+    """Per-system FGMRES state (the locals of fgmres.py:31-131).  The Krylov
+    bases live in the batched tensors V [B, mr+1, n], Z [B, mr, n]."""
 
-    def __init__(self, n, mr, dtype, device, npdt):
-        self.mr = mr
-        self.V = torch.zeros((mr + 1, n), dtype=dtype, device=device)
-        self.Z = torch.zeros((mr, n), dtype=dtype, device=device)
-        self.npdt = npdt
+    def __init__(self, b, V, Z, mr, npdt):
+        self.b, self.V, self.Z, self.mr, self.npdt = b, V, Z, mr, npdt
         self.trace = []
         self.total = 0
         self.outer = 0
@@ -61,15 +59,19 @@ class _Sys:
         self.cs = np.zeros(mr, dtype=dt)
         self.sn = np.zeros(mr, dtype=dt)
         self.g = np.zeros(mr + 1, dtype=dt)
-        self.V.zero_()
-        self.Z.zero_()
-        self.V[0] = r / beta
+        self.V[self.b].zero_()
+        self.Z[self.b].zero_()
+        self.V[self.b, 0] = r / beta
         self.g[0] = beta
         self.k = 0
 
 
 def fgmres_batched(A, F, precond_apply=None, cfg: FgmresConfig = None, U0=None):
-    """B independent FGMRES solves sharing batched operator/preconditioner calls."""
+    """B independent FGMRES solves sharing batched operator/preconditioner
+    calls.  Modified Gram-Schmidt is vectorised across the systems that sit
+    at the same Arnoldi index (the common case): per orthogonalisation index
+    one batched dot and one batched update for all of them, each system
+    still orthogonalised in the reference's order (fgmres.py:76-78)."""
     cfg = cfg or FgmresConfig()
     op = A if isinstance(A, GpuStencilOperator) else _op_for(A, F)
     host = _is_host(F)
@@ -77,10 +79,13 @@ def fgmres_batched(A, F, precond_apply=None, cfg: FgmresConfig = None, U0=None):
     B, n = op.batch, op.P
     Fd = op.to_device(F)
     npdt = op.np_dtype
+    mr = cfg.restart
     precond = precond_apply if precond_apply is not None else (lambda r: r)
     U = torch.zeros_like(Fd) if U0 is None else op.to_device(U0).clone()
+    V = torch.zeros((B, mr + 1, n), dtype=op.torch_dtype, device=op.device)
+    Z = torch.zeros((B, mr, n), dtype=op.torch_dtype, device=op.device)
     fn = torch.linalg.vector_norm(Fd, dim=1).cpu().numpy()
-    systems = [_Sys(n, cfg.restart, op.torch_dtype, op.device, npdt) for _ in range(B)]
+    systems = [_Sys(b, V, Z, mr, npdt) for b in range(B)]
     Rr = Fd - _matvec(op, U)
     beta = torch.linalg.vector_norm(Rr, dim=1).cpu().numpy()
     for b, s in enumerate(systems):
@@ -96,32 +101,44 @@ def fgmres_batched(A, F, precond_apply=None, cfg: FgmresConfig = None, U0=None):
             s.start_cycle(Rr[b], float(beta[b]))
     while not all(s.done for s in systems):
         # ---- one Arnoldi step for every running system (fgmres.py:349-385)
-        Vk = torch.stack([s.V[s.k] if not s.done else torch.zeros_like(Fd[0]) for s in systems])
+        run = [s for s in systems if not s.done]
+        ks = torch.tensor([s.k if not s.done else 0 for s in systems], device=op.device)
+        Vk = V[torch.arange(B, device=op.device), ks]
+        for s in systems:
+            if s.done:
+                Vk[s.b].zero_()
         Zk = precond(Vk)
         Zk = (Zk if isinstance(Zk, torch.Tensor) else torch.as_tensor(np.asarray(Zk))).to(
             op.device, op.torch_dtype).reshape(B, n)
         W = _matvec(op, Zk)
-        cols = []
-        for b, s in enumerate(systems):
-            if s.done:
-                cols.append(None)
-                continue
-            k = s.k
-            s.Z[k] = Zk[b]
-            w = W[b].clone()
-            hcol = []
-            for i in range(k + 1):              # modified Gram-Schmidt (:76-78)
-                h = torch.vdot(s.V[i], w)
-                w = w - h * s.V[i]
-                hcol.append(h)
-            hk1 = torch.linalg.vector_norm(w)
-            s._w = w
-            cols.append((torch.stack(hcol), hk1))
-        host_cols = [None if c is None else (c[0].cpu().numpy(), float(c[1].item())) for c in cols]
-        for b, s in enumerate(systems):
-            if s.done:
-                continue
-            hc, hk1 = host_cols[b]
+        hcols, hk1s = {}, {}
+        # group running systems by Arnoldi index
+        groups = {}
+        for s in run:
+            groups.setdefault(s.k, []).append(s.b)
+        for k, bs in groups.items():
+            full = len(bs) == B
+            idx = None if full else torch.tensor(bs, device=op.device)
+            w = W if full else W.index_select(0, idx)       # [G, n]
+            if full:
+                Z[:, k] = Zk
+            else:
+                Z[idx, k] = Zk.index_select(0, idx)
+            hs = []
+            for i in range(k + 1):                          # modified Gram-Schmidt (:76-78)
+                vi = V[:, i] if full else V[idx, i]
+                h = torch.linalg.vecdot(vi, w)              # conj(v_i) . w  (np.vdot)
+                w = w - h[:, None] * vi
+                hs.append(h)
+            hk1 = torch.linalg.vector_norm(w, dim=1)
+            H = torch.stack(hs, dim=1)                       # [G, k+1]
+            for q, b in enumerate(bs):
+                hcols[b] = H[q]
+                hk1s[b] = hk1[q]
+                systems[b]._w = w[q]
+        hcol_h = {b: (hcols[b].cpu().numpy(), float(hk1s[b].item())) for b in hcols}
+        for s in run:
+            hc, hk1 = hcol_h[s.b]
             k, H, cs, sn, g = s.k, s.H, s.cs, s.sn, s.g
             H[:k + 1, k] = hc
             H[k + 1, k] = hk1
@@ -144,16 +161,15 @@ def fgmres_batched(A, F, precond_apply=None, cfg: FgmresConfig = None, U0=None):
             s.trace.append(s.rel)
             happy = hk1 <= 1e-14 * max(1.0, float(np.abs(H[k, k])))
             s.k = k + 1
-            end_cycle = False
             if s.rel <= cfg.tol or happy:
                 s.converged = True
                 end_cycle = True
             else:
                 if hk1 > 0:
-                    s.V[s.k] = s._w / hk1
+                    V[s.b, s.k] = s._w / hk1
                 end_cycle = s.k >= s.mr
             if end_cycle:
-                _finish_cycle(op, Fd, U, b, s, cfg)
+                _finish_cycle(op, Fd, U, s.b, s, cfg)
     wall = time.perf_counter() - t0
     Uo = U.cpu().numpy() if host else U
     return [(Uo[b], SolveReport(iterations=s.total, inner_iterations=s.total,
@@ -174,7 +190,7 @@ def _finish_cycle(op, Fd, U, b, s, cfg):
         except np.linalg.LinAlgError:
             y = np.linalg.lstsq(Hk, s.g[:k], rcond=None)[0]
     yt = torch.as_tensor(y).to(U.device, U.dtype)
-    U[b] = U[b] + yt @ s.Z[:k]
+    U[b] = U[b] + yt @ s.Z[b, :k]
     r = Fd[b] - _matvec_one(op, U, b)
     beta = float(torch.linalg.vector_norm(r).item())
     s.rel = beta / s.fnorm
