@@ -174,6 +174,17 @@ int rg_prolong_add(int dtype, int batch, int n, const void* coarse, void* fine,
 int rg_dense_apply(int dtype, int batch, int n, const void* M, int shared,
                    const void* x, void* y, void* stream);
 
+/* ---- FGMRES building block (fgmres.py:76-78) -------------------------------
+ * One fused modified Gram-Schmidt index for `batch` systems (vectors of n
+ * float64 / complex128, system b at w + b*ldw etc.):
+ *     w -= h[b] * v          (skipped when v is NULL)
+ *     hn[b] = vdot(vn, w)    (skipped when vn is NULL; conj(vn) . w)
+ *     wnorm2[b] = ||w||^2    (when wnorm2 is not NULL)
+ * h, hn, wnorm2 are device arrays [batch]. */
+int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void* v,
+                long long ldv, const void* h, const void* vn, long long ldvn, void* hn,
+                double* wnorm2, void* stream);
+
 /* ---- solve_stationary engine (richardson.py:77-141) ----------------------
  * A solver owns device workspace (per-system status, trace, reduction
  * partials) and runs the whole loop on the device: convergence, divergence

@@ -60,6 +60,8 @@ _SIGS = [
     ("rg_restrict", _I, [_I, _I, _I, _P, _P, _P]),
     ("rg_prolong_add", _I, [_I, _I, _I, _P, _P, _P]),
     ("rg_dense_apply", _I, [_I, _I, _I, _P, _I, _P, _P, _P]),
+    ("rg_mgs_step", _I, [_I, _I, _I, _P, C.c_longlong, _P, C.c_longlong, _P, _P, C.c_longlong, _P,
+                         _P, _P]),
     ("rg_solver_create", _I, [C.POINTER(_P), _P, C.POINTER(rg_sched), C.c_double, _I, _I, _I]),
     ("rg_solver_destroy", _I, [_P]),
     ("rg_solver_begin", _I, [_P, _P, _P, _P, _P, _P, _P]),

@@ -16,6 +16,7 @@
 #include "dst.cuh"
 #include "mg.cuh"
 #include "cluster.cuh"
+#include "krylov.cuh"
 
 using namespace rg;
 
@@ -635,6 +636,37 @@ int rg_dense_apply(int dtype, int batch, int n, const void* M, int shared, const
     else if (dtype == RG_F32) dense_apply_kernel<float><<<g, 256, 0, st>>>((const float*)M, shared, (const float*)x, (float*)y, n);
     else dense_apply_kernel<double2><<<g, 256, 0, st>>>((const double2*)M, shared, (const double2*)x, (double2*)y, n);
     LAUNCH_CHECK();
+    return RG_OK;
+}
+
+int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void* v, long long ldv,
+                const void* h, const void* vn, long long ldvn, void* hn, double* wnorm2,
+                void* stream) {
+    if (!w) return fail(RG_ENULL, "null w");
+    if (dtype != RG_F64 && dtype != RG_C128) return fail(RG_EINVAL, "mgs: float64 or complex128");
+    if (batch < 1 || n < 1) return fail(RG_ESIZE, "bad size");
+    if (v && !h) return fail(RG_ENULL, "projection needs h");
+    if (vn && !hn) return fail(RG_ENULL, "dot needs hn");
+    cudaStream_t st = (cudaStream_t)stream;
+    int ncta = (n + MGS_NT * 4 - 1) / (MGS_NT * 4);
+    if (ncta > 512) ncta = 512;
+    double* part = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double) * 3 * ncta * batch, st));
+    const dim3 g(ncta, batch);
+    if (dtype == RG_F64) {
+        MgsArgs<double> a{(double*)w, ldw, (const double*)v, ldv, (const double*)h,
+                          (const double*)vn, ldvn, part, n, wnorm2 != nullptr};
+        mgs_kernel<double><<<g, MGS_NT, 0, st>>>(a);
+        mgs_finish_kernel<double><<<batch, MGS_NT, 0, st>>>(part, ncta, (double*)hn, wnorm2);
+    } else {
+        MgsArgs<double2> a{(double2*)w, ldw, (const double2*)v, ldv, (const double2*)h,
+                           (const double2*)vn, ldvn, part, n, wnorm2 != nullptr};
+        mgs_kernel<double2><<<g, MGS_NT, 0, st>>>(a);
+        mgs_finish_kernel<double2><<<batch, MGS_NT, 0, st>>>(part, ncta, (double2*)hn, wnorm2);
+    }
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(part, st);
+    if (e != cudaSuccess) return fail(RG_ECUDA, "mgs launch: %s", cudaGetErrorString(e));
     return RG_OK;
 }
 

@@ -20,6 +20,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from . import _lib as L
 from .errors import SolveReport
 from .operator import GpuStencilOperator
 from .richardson import _is_host, _op_for
@@ -119,19 +120,37 @@ def fgmres_batched(A, F, precond_apply=None, cfg: FgmresConfig = None, U0=None):
         for k, bs in groups.items():
             full = len(bs) == B
             idx = None if full else torch.tensor(bs, device=op.device)
-            w = W if full else W.index_select(0, idx)       # [G, n]
             if full:
                 Z[:, k] = Zk
+                # modified Gram-Schmidt (:76-78) with the fused device kernel:
+                # one pass per index applies the previous projection and takes
+                # the next inner product (rg_mgs_step)
+                w = W.contiguous()
+                hbuf = torch.empty((k + 1, B), dtype=op.torch_dtype, device=op.device)
+                n2 = torch.empty(B, dtype=torch.float64, device=op.device)
+                ld = (mr + 1) * n
+                code = L.RG_C128 if op.torch_dtype == torch.complex128 else L.RG_F64
+                for i in range(k + 1):
+                    L.check(op._lib.rg_mgs_step(
+                        code, B, n, L.ptr(w), n,
+                        L.ptr(V[:, i - 1]) if i else None, ld, L.ptr(hbuf[i - 1]) if i else None,
+                        L.ptr(V[:, i]), ld, L.ptr(hbuf[i]), None, L.stream_ptr()))
+                L.check(op._lib.rg_mgs_step(code, B, n, L.ptr(w), n, L.ptr(V[:, k]), ld,
+                                            L.ptr(hbuf[k]), None, 0, None, L.ptr(n2),
+                                            L.stream_ptr()))
+                hk1 = torch.sqrt(n2)
+                H = hbuf.t()                                  # [G, k+1]
             else:
+                w = W.index_select(0, idx)                    # [G, n]
                 Z[idx, k] = Zk.index_select(0, idx)
-            hs = []
-            for i in range(k + 1):                          # modified Gram-Schmidt (:76-78)
-                vi = V[:, i] if full else V[idx, i]
-                h = torch.linalg.vecdot(vi, w)              # conj(v_i) . w  (np.vdot)
-                w = w - h[:, None] * vi
-                hs.append(h)
-            hk1 = torch.linalg.vector_norm(w, dim=1)
-            H = torch.stack(hs, dim=1)                       # [G, k+1]
+                hs = []
+                for i in range(k + 1):                        # modified Gram-Schmidt (:76-78)
+                    vi = V[idx, i]
+                    h = torch.linalg.vecdot(vi, w)            # conj(v_i) . w  (np.vdot)
+                    w = w - h[:, None] * vi
+                    hs.append(h)
+                hk1 = torch.linalg.vector_norm(w, dim=1)
+                H = torch.stack(hs, dim=1)                     # [G, k+1]
             for q, b in enumerate(bs):
                 hcols[b] = H[q]
                 hk1s[b] = hk1[q]

@@ -44,3 +44,11 @@ torch.cuda.synchronize()
 tot = time.perf_counter() - t0
 print(f"20 Arnoldi steps: total {1e3*tot:.1f} ms  precond {1e3*T['precond']:.1f} ms  "
       f"matvec {1e3*T['matvec']:.1f} ms  rest {1e3*(tot-T['precond']-T['matvec']):.1f} ms")
+
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    GG.fgmres_batched(op, Fd, precond_apply=lambda R: h.apply(R),
+                      cfg=GG.FgmresConfig(restart=6, tol=1e-6, max_outer=1))
+    torch.cuda.synchronize()
+print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=14))
+print(prof.key_averages().table(sort_by="cpu_time_total", row_limit=14))
