@@ -17,6 +17,7 @@
 #include "mg.cuh"
 #include "cluster.cuh"
 #include "krylov.cuh"
+#include "cblock.cuh"
 
 using namespace rg;
 
@@ -52,6 +53,8 @@ struct rg_op {
     rg_op_desc d;
     int P;
     std::vector<double> hcoef;   // CONST9 real: host copy of [batch][9] (kernel params)
+    bool cblock_ok = false;      // DIAG5 c128 with one set of off-diagonals: blocked sweep
+    double2 hoff[4];
 };
 
 struct rg_solver {
@@ -372,6 +375,19 @@ int rg_op_create(rg_op** out, const rg_op_desc* d) {
                 for (int q = 0; q < 9; ++q) A->hcoef[(size_t)b * 9 + q] = A->hcoef[q];
         }
     }
+    if (d->kind == RG_DIAG5 && d->dtype == RG_C128) {
+        const int nsets = d->shared ? 1 : d->batch;
+        std::vector<double2> off((size_t)nsets * 4);
+        if (cudaMemcpy(off.data(), d->stencil, off.size() * sizeof(double2), cudaMemcpyDeviceToHost) ==
+            cudaSuccess) {
+            bool same = true;
+            for (int b = 1; b < nsets && same; ++b)
+                for (int q = 0; q < 4; ++q)
+                    same = same && off[b * 4 + q].x == off[q].x && off[b * 4 + q].y == off[q].y;
+            A->cblock_ok = same;
+            for (int q = 0; q < 4; ++q) A->hoff[q] = off[q];
+        }
+    }
     *out = A;
     return RG_OK;
 }
@@ -482,6 +498,8 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     const bool real = A->d.dtype == RG_F32 || A->d.dtype == RG_F64;
     const bool blocked = real && A->d.kind == RG_CONST9 &&
                          s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
+    // complex 5-point Helmholtz smoother (V-cycle fine level): blocked sweep
+    const bool cblocked = !blocked && A->cblock_ok && s->precond == RG_PRECOND_NONE && block_T != 1;
     std::vector<double> hscale;
     const bool jac = s->precond == RG_PRECOND_JACOBI_SCALAR;
     if (blocked && jac) {
@@ -493,9 +511,35 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     const int T = block_T == 0 ? 5 : block_T;
     int k = i0;
     int left = n_steps;
+    const int TC = block_T == 0 ? 4 : (block_T < 4 ? block_T : 4);
     while (left > 0) {
-        const int t = blocked ? chunk_len(n_steps, T, n_steps - left) : 1;
-        if (blocked) {
+        const int t = blocked ? chunk_len(n_steps, T, n_steps - left)
+                              : (cblocked ? chunk_len(n_steps, TC, n_steps - left) : 1);
+        if (cblocked) {
+            CBlockArgs ca;
+            for (int q = 0; q < 4; ++q) ca.off[q] = A->hoff[q];
+            ca.diag = (const double2*)A->d.diag;
+            ca.diag_shared = A->d.shared;
+            ca.side = A->d.side;
+            ca.P = A->P;
+            ca.u_in = (const double2*)u[cur];
+            ca.u_out = (double2*)u[cur ^ 1];
+            ca.v_in = (const double2*)v[cur];
+            ca.v_out = (double2*)v[cur ^ 1];
+            ca.f = (const double2*)f;
+            ca.omega = s->omega;
+            ca.alpha = s->alpha;
+            ca.atil = s->alpha_tilde;
+            ca.m = s->m;
+            ca.k0 = k;
+            cudaError_t err;
+            switch (s->variant) {
+                case RG_PLAIN: err = launch_cblock<V_PLAIN>(ca, t, A->d.batch, st); break;
+                case RG_MOM: err = launch_cblock<V_MOM>(ca, t, A->d.batch, st); break;
+                default: err = launch_cblock<V_NAG>(ca, t, A->d.batch, st); break;
+            }
+            rc = err == cudaSuccess ? RG_OK : fail(RG_ECUDA, "complex sweep launch: %s", cudaGetErrorString(err));
+        } else if (blocked) {
             rc = A->d.dtype == RG_F64
                      ? sweep_block<double>(A, s, k, t, jac, hscale, u[cur], u[cur ^ 1], v[cur], v[cur ^ 1], f, st)
                      : sweep_block<float>(A, s, k, t, jac, hscale, u[cur], u[cur ^ 1], v[cur], v[cur ^ 1], f, st);

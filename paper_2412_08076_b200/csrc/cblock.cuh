@@ -1,0 +1,183 @@
+// cblock.cuh — temporally blocked free-running sweeps for the complex
+// 5-point damped-Helmholtz operator (DIAG5, complex128), the V-cycle fine
+// level smoother of cfg5 (multigrid.py:126-138: plain/mom/nag, fresh v, no
+// preconditioner).
+//
+// Same overlapped-tile scheme as block.cuh: one CTA owns an LR x LC window
+// with a T-cell halo and runs T inner steps on chip.  The stencil input (u,
+// or the look-ahead y = u + at v) is ping-ponged in shared memory as
+// complex128, f of the window sits in shared memory, the per-node complex
+// diagonal is read through L1 (it is shared by every right-hand side of the
+// batch, so it stays L2/L1 resident), u and v of the thread's points live in
+// registers.  Products are the unfused complex formula in CSR column order
+// (-1,0),(0,-1),(0,0),(0,1),(1,0): bitwise equal to the CSR matvec.
+#pragma once
+#include "step.cuh"
+
+namespace rg {
+
+constexpr int CB_LR = 32, CB_LC = 64, CB_NW = 8;
+
+struct CBlockArgs {
+    double2 off[4];        // off-diagonals in CSR order (-1,0),(0,-1),(0,1),(1,0)
+    const double2* diag;   // [P] (shared operator) or [B][P]
+    int diag_shared;
+    int side, P;
+    const double2* u_in;
+    const double2* v_in;
+    double2* u_out;
+    double2* v_out;
+    const double2* f;
+    const double* omega;
+    const double* alpha;
+    const double* atil;
+    int m;
+    int k0;
+    int nty;
+};
+
+__host__ __device__ inline int cblock_ntiles(int side, int T, int* nty) {
+    const int TX = CB_LR - 2 * T, TY = CB_LC - 2 * T;
+    const int ny = (side + TY - 1) / TY;
+    if (nty) *nty = ny;
+    return ((side + TX - 1) / TX) * ny;
+}
+
+template <int VAR, int T>
+__global__ void __launch_bounds__(CB_NW * 32, 2) cblock_kernel(const __grid_constant__ CBlockArgs a) {
+    typedef double2 C;
+    constexpr int LR = CB_LR, LC = CB_LC;
+    constexpr int RPW = LR / CB_NW, CPT = LC / 32;
+    constexpr int TX = LR - 2 * T, TY = LC - 2 * T;
+    constexpr bool NAG = VAR >= V_NAG;
+    constexpr bool HASV = VAR != V_PLAIN;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typedef C Row[LC];
+    Row* buf0 = reinterpret_cast<Row*>(smem_raw);
+    Row* buf1 = buf0 + LR;
+    Row* sf = buf1 + LR;
+
+    const int b = blockIdx.y;
+    const int cta = blockIdx.x;
+    const int tx = cta / a.nty, ty = cta - (cta / a.nty) * a.nty;
+    const int gx0 = tx * TX - T, gy0 = ty * TY - T;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int side = a.side;
+    const size_t base = (size_t)b * a.P;
+    const double2* dg = a.diag + (a.diag_shared ? 0 : base);
+    const int r0 = wp * RPW;
+    const C c0 = a.off[0], c1 = a.off[1], c2 = a.off[2], c3 = a.off[3];
+
+    C ur[RPW][CPT], vr[RPW][CPT];
+    int gidx[RPW][CPT];       // global index of the point, -1 outside the grid
+    const double at0 = NAG ? a.atil[b * a.m + (a.k0 % a.m)] : 0.0;
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+        const int gx = gx0 + r0 + rr;
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int col = lane + 32 * cc;
+            const int gy = gy0 + col;
+            const bool in = (gx >= 0) && (gx < side) && (gy >= 0) && (gy < side);
+            const int g = in ? gx * side + gy : -1;
+            gidx[rr][cc] = g;
+            const C u = in ? a.u_in[base + g] : szero<C>();
+            const C v = (HASV && in) ? a.v_in[base + g] : szero<C>();
+            ur[rr][cc] = u;
+            vr[rr][cc] = v;
+            sf[r0 + rr][col] = in ? a.f[base + g] : szero<C>();
+            buf0[r0 + rr][col] = (NAG && in) ? add(u, rmul(at0, v)) : u;   // (:119)
+        }
+    }
+    __syncthreads();
+
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int k = a.k0 + t;
+        const int si = b * a.m + (k % a.m);
+        const double w = a.omega[si];
+        const double al = HASV ? a.alpha[si] : 0.0;
+        const double atn = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+        Row* cur = (t & 1) ? buf1 : buf0;
+        Row* nxt = (t & 1) ? buf0 : buf1;
+        const bool last = (t == T - 1);
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int col = lane + 32 * cc;
+            const int cm = col > 0 ? col - 1 : 0;
+            const int cp = col < LC - 1 ? col + 1 : LC - 1;
+            const int rm = r0 > 0 ? r0 - 1 : 0;
+            C up = cur[rm][col];
+            C mid = cur[r0][col];
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) {
+                const int r = r0 + rr;
+                const int rp = r + 1 < LR ? r + 1 : LR - 1;
+                const C wv = cur[r][cm], ev = cur[r][cp], dn = cur[rp][col];
+                const int g = gidx[rr][cc];
+                const C d = g >= 0 ? __ldg(&dg[g]) : szero<C>();
+                C s = mul(c0, up);                        // CSR order, unfused products
+                s = add(s, mul(c1, wv));
+                s = add(s, mul(d, mid));
+                s = add(s, mul(c2, ev));
+                s = add(s, mul(c3, dn));
+                const C rs = sub(sf[r][col], s);          // r = f - A x
+                C vn;
+                if (VAR == V_PLAIN) vn = rmul(w, rs);
+                else vn = add(rmul(al, vr[rr][cc]), rmul(w, rs));   // v = a v + w r
+                const C un = add(NAG ? ur[rr][cc] : mid, vn);      // u = u + v
+                if (HASV) vr[rr][cc] = vn;
+                ur[rr][cc] = un;
+                if (!last) {
+                    const C x = NAG ? add(un, rmul(atn, vn)) : un;
+                    nxt[r][col] = g >= 0 ? x : szero<C>();
+                }
+                up = mid;
+                mid = dn;
+            }
+        }
+        if (!last) __syncthreads();
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+        const int r = r0 + rr;
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int col = lane + 32 * cc;
+            const int g = gidx[rr][cc];
+            if (g >= 0 && r >= T && r < LR - T && col >= T && col < LC - T) {
+                a.u_out[base + g] = ur[rr][cc];
+                if (HASV) a.v_out[base + g] = vr[rr][cc];
+            }
+        }
+    }
+}
+
+template <int VAR, int T>
+cudaError_t launch_cblock_t(const CBlockArgs& a0, int batch, cudaStream_t st) {
+    auto kern = cblock_kernel<VAR, T>;
+    const size_t smem = 3 * (size_t)CB_LR * CB_LC * sizeof(double2);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    CBlockArgs a = a0;
+    const int nt = cblock_ntiles(a.side, T, &a.nty);
+    kern<<<dim3(nt, batch), dim3(CB_NW * 32), smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int VAR>
+cudaError_t launch_cblock(const CBlockArgs& a, int T, int batch, cudaStream_t st) {
+    switch (T) {
+        case 1: return launch_cblock_t<VAR, 1>(a, batch, st);
+        case 2: return launch_cblock_t<VAR, 2>(a, batch, st);
+        case 3: return launch_cblock_t<VAR, 3>(a, batch, st);
+        case 4: return launch_cblock_t<VAR, 4>(a, batch, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace rg

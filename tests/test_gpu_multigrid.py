@@ -106,3 +106,56 @@ def test_fgmres_plain_matches_oracle():
     assert rep.iterations == ro["iterations"]
     assert np.allclose(rep.trace, ro["trace"], rtol=1e-7, atol=0)
     assert _rel(u, uo) <= 1e-7
+
+
+def _csweep(op, variant, n_steps, block_T, f, u0, v0, seed=0):
+    """rg_sweep on a complex DIAG5 operator, returns (u, v) on the host."""
+    import ctypes as C
+    m = 4
+    rng = np.random.default_rng(seed)
+    lam = 8.0 * op.side ** 2
+    w = rng.uniform(0.2, 0.9, m) / lam
+    kw = {} if variant == "plain" else {"alpha": np.full(m, 0.35)}
+    from paper_2412_08076_b200.richardson import DeviceSchedule
+    sch = DeviceSchedule(op, G.WeightSchedule(omega=w, variant=variant, **kw))
+    dev = op.device
+    t = lambda a: torch.as_tensor(a).to(dev).clone()
+    u = [t(u0), torch.empty_like(t(u0))]
+    v = [t(v0), torch.empty_like(t(v0))]
+    fd = t(f)
+    outb = C.c_int()
+    L.check(L.load().rg_sweep(op.handle, C.byref(sch.struct), 0, n_steps, block_T,
+                             L.ptr(u[0]), L.ptr(u[1]), L.ptr(v[0]), L.ptr(v[1]), L.ptr(fd),
+                             C.byref(outb), L.stream_ptr()))
+    torch.cuda.synchronize()
+    return u[outb.value].cpu().numpy(), v[outb.value].cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [9, 101, 258])
+@pytest.mark.parametrize("variant", ["plain", "mom", "nag"])
+def test_complex_blocked_sweep_bitwise(n, variant):
+    """The temporally blocked complex 5-point sweep (cblock.cuh, the V-cycle
+    fine-level smoother) gives the one-step kernel's bits at every depth."""
+    A = O.assemble_helmholtz(12.0, n)
+    B = 3
+    op = G.GpuStencilOperator.from_sparse(A).broadcast(B)
+    rng = np.random.default_rng(n)
+    P = A.shape[0]
+    cplx = lambda: rng.standard_normal((B, P)) + 1j * rng.standard_normal((B, P))
+    f, u0 = cplx(), cplx()
+    v0 = cplx() if variant != "plain" else np.zeros((B, P), complex)
+    ref = _csweep(op, variant, 11, 1, f, u0, v0)
+    for T in (0, 2, 3, 4):
+        got = _csweep(op, variant, 11, T, f, u0, v0)
+        assert np.array_equal(got[0], ref[0]), (T, np.abs(got[0] - ref[0]).max())
+        if variant != "plain":
+            assert np.array_equal(got[1], ref[1])
+    # and the one-step path is the CSR loop of the reference (system 1)
+    s = G.WeightSchedule(omega=np.random.default_rng(0).uniform(0.2, 0.9, 4) / (8.0 * op.side ** 2),
+                         variant=variant, **({} if variant == "plain" else {"alpha": np.full(4, 0.35)}))
+    if variant != "plain":
+        return
+    x = u0[1].copy()
+    for k in range(11):
+        x = x + s.omega[k % 4] * (f[1] - A @ x)
+    assert np.array_equal(ref[0][1], x)
