@@ -185,6 +185,26 @@ int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void*
                 long long ldv, const void* h, const void* vn, long long ldvn, void* hn,
                 double* wnorm2, void* stream);
 
+/* ---- Gauss-Seidel / SOR / SSOR preconditioners (precond.py:79-118) --------
+ * z = B^{-1} r for every system of a CONST9 real operator:
+ *   RG_TRI_SOR  : z = relax (D + relax L)^{-1} r          (gauss_seidel: relax 1)
+ *   RG_TRI_SSOR : z = c (D + relax U)^{-1} D (D + relax L)^{-1} r,
+ *                 c = relax (2 - relax)
+ * L, U: strict lower / upper parts of A in lexicographic order.  Replaces the
+ * SuperLU triangular solves of precond.py:36-45 (agreement to rounding,
+ * ~1e-15; the reference's own bar is 1e-13).  relax in (0, 2); a zero
+ * diagonal is RG_EINVAL (ZeroDiagonalError).  work: [batch][side*side]
+ * scratch for SSOR (may be NULL for SOR).  r and z must not alias. */
+enum rg_tri { RG_TRI_SOR = 1, RG_TRI_SSOR = 2 };
+int rg_tri_apply(const rg_op* A, int kind, double relax, const void* r, void* z,
+                 void* work, void* stream);
+/* The Richardson update from an externally preconditioned residual z
+ * (richardson.py:120-121): v = a_i v + w_i z; u = u + v (in place), and when
+ * y != NULL the next look-ahead y = u + at_{(i+1) mod m} v (nag/nagex).
+ * z == NULL: only y = u + at_i v.  v may be NULL for plain. */
+int rg_precond_update(const rg_op* A, const rg_sched* s, int i, const void* z,
+                      void* u, void* v, void* y, void* stream);
+
 /* ---- solve_stationary engine (richardson.py:77-141) ----------------------
  * A solver owns device workspace (per-system status, trace, reduction
  * partials) and runs the whole loop on the device: convergence, divergence

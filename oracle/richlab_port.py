@@ -15,6 +15,7 @@ import numpy as np
 import scipy.fft
 import scipy.linalg
 import scipy.sparse as sp
+import scipy.sparse.linalg as spla
 
 DIVERGENCE_FACTOR = 1e12  # richardson.py:17
 
@@ -116,6 +117,43 @@ def jacobi_scale(A, relax=2.0 / 3.0):
     return relax / A.diagonal()
 
 
+def _tri_solver(T):
+    """precond.py:36-45: SuperLU of a triangular matrix in natural order
+    without pivoting (the factor is the matrix itself), used as a
+    substitution routine."""
+    lu = spla.splu(T.tocsc(), permc_spec="NATURAL", diag_pivot_thresh=0.0,
+                   options={"SymmetricMode": True})
+    return lu.solve
+
+
+def tri_precond(A, kind, relax=1.0):
+    """precond.py:79-118: r -> B^{-1} r for kind 'gauss-seidel' (relax 1),
+    'sor' or 'ssor'.  A: scipy CSR."""
+    if kind == "gauss-seidel":
+        relax = 1.0
+    if not 0.0 < relax < 2.0:
+        raise ValueError(f"relaxation must be in (0, 2), got {relax}")
+    diag = A.diagonal()
+    if np.any(diag == 0):
+        raise ValueError(f"zero diagonal entry in row {int(np.nonzero(diag == 0)[0][0])}")
+    DL = (sp.diags(diag) + relax * sp.tril(A, k=-1)).tocsr()
+    dl = _tri_solver(DL)
+    if kind in ("sor", "gauss-seidel"):
+        return lambda r: relax * dl(r)
+    DU = (sp.diags(diag) + relax * sp.triu(A, k=1)).tocsr()
+    du = _tri_solver(DU)
+    c = relax * (2.0 - relax)
+    return lambda r: c * du(diag * dl(r))
+
+
+def _precond(scale, r):
+    """apply_preconditioner (precond.py:125-129): None, a Jacobi scale
+    array, or a callable map."""
+    if scale is None:
+        return r
+    return scale(r) if callable(scale) else scale * r
+
+
 def _norm(x):
     return float(np.linalg.norm(x))
 
@@ -127,7 +165,7 @@ def inner_update(A, f, u, v, w, a, at, variant, scale=None):
         r = f - A.dot(u)
     else:
         r = f - A.dot(u + at * v)
-    p = r if scale is None else scale * r
+    p = _precond(scale, r)
     v = a * v + w * p
     return u + v, v
 
@@ -157,7 +195,7 @@ def solve_stationary(A, f, omega, alpha=None, alpha_tilde=None, variant="plain",
         for i in range(m):
             w, a, at = omega[i], alpha[i], alpha_tilde[i]
             step_r = r if reuse else f - A.dot(u + at * v)
-            p = step_r if scale is None else scale * step_r
+            p = _precond(scale, step_r)
             v = a * v + w * p
             u = u + v
             inner += 1

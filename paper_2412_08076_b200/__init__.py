@@ -11,6 +11,7 @@ that mirrors the reference API.
 from .errors import (DIVERGENCE_FACTOR, DimensionMismatch, DivergenceError, IterationState,
                      ShannonViolation, SolveReport, UnsupportedOperator, ZeroDiagonalError)
 from .operator import GpuStencilOperator, JacobiScale, as_operator
+from .precond import Preconditioner, TriangularPreconditioner
 from .problems import (AnisotropicProblem, HelmholtzProblem, anisotropic_stencil,
                        helmholtz_stencil)
 from .richardson import (StationarySolver, inner_update, outer_sweep, solve_stationary,

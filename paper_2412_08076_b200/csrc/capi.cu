@@ -18,6 +18,7 @@
 #include "cluster.cuh"
 #include "krylov.cuh"
 #include "cblock.cuh"
+#include "tri.cuh"
 
 using namespace rg;
 
@@ -480,6 +481,64 @@ int rg_inner_update(const rg_op* A, const rg_sched* s, int i, const void* u_in, 
     q.nonfinite_at = nonfinite_at;
     q.tag = tag;
     return step1(A, q, (cudaStream_t)stream);
+}
+
+int rg_tri_apply(const rg_op* A, int kind, double relax, const void* r, void* z, void* work,
+                 void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if (A->d.kind != RG_CONST9 || A->d.dtype == RG_C128)
+        return fail(RG_EUNSUPPORTED, "GS/SOR/SSOR need a CONST9 real operator");
+    if (kind != RG_TRI_SOR && kind != RG_TRI_SSOR) return fail(RG_EINVAL, "bad triangular kind %d", kind);
+    if (!(relax > 0.0 && relax < 2.0)) return fail(RG_EINVAL, "relaxation must be in (0, 2), got %g", relax);
+    if (!r || !z || (kind == RG_TRI_SSOR && !work)) return fail(RG_ENULL, "null vector");
+    if (r == z || work == r || work == z) return fail(RG_EINVAL, "r, z and work must not alias");
+    for (int b = 0; b < (A->d.shared ? 1 : A->d.batch); ++b)
+        if (A->hcoef[(size_t)b * 9 + 4] == 0.0) return fail(RG_EINVAL, "zero diagonal entry in system %d", b);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if (A->d.dtype == RG_F64) {
+        TriArgs<double> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P, relax,
+                          (const double*)r, (double*)z, (double*)work};
+        e = launch_tri(a, kind, A->d.batch, st);
+    } else {
+        TriArgs<float> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P, relax,
+                         (const float*)r, (float*)z, (float*)work};
+        e = launch_tri(a, kind, A->d.batch, st);
+    }
+    return e == cudaSuccess ? RG_OK : fail(RG_ECUDA, "triangular solve launch: %s", cudaGetErrorString(e));
+}
+
+int rg_precond_update(const rg_op* A, const rg_sched* s, int i, const void* z, void* u, void* v,
+                      void* y, void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if ((rc = check_sched(A, s))) return rc;
+    if (i < 0 || i >= s->m) return fail(RG_EINVAL, "inner index %d outside [0, %d)", i, s->m);
+    if (!u) return fail(RG_ENULL, "null u");
+    if (s->variant != RG_PLAIN && !v) return fail(RG_ENULL, "variant needs v");
+    if (!z && !y) return fail(RG_ENULL, "nothing to compute");
+    if ((y || !z) && !s->alpha_tilde) return fail(RG_ENULL, "look-ahead needs alpha_tilde");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)A->d.batch * A->P;
+    const int nb = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+    const int var = s->variant;
+    switch (A->d.dtype) {
+        case RG_F64:
+            pupdate_kernel<double><<<nb, 256, 0, st>>>(A->d.batch, A->P, (const double*)z, (double*)u,
+                                                      (double*)v, (double*)y, s->omega, s->alpha,
+                                                      s->alpha_tilde, s->m, i, var);
+            break;
+        case RG_F32:
+            pupdate_kernel<float><<<nb, 256, 0, st>>>(A->d.batch, A->P, (const float*)z, (float*)u,
+                                                     (float*)v, (float*)y, s->omega, s->alpha,
+                                                     s->alpha_tilde, s->m, i, var);
+            break;
+        default:
+            return fail(RG_EUNSUPPORTED, "external-preconditioner update needs a real operator");
+    }
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RG_OK : fail(RG_ECUDA, "update launch: %s", cudaGetErrorString(e));
 }
 
 int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,

@@ -26,6 +26,7 @@ import torch
 from . import _lib as L
 from .errors import DimensionMismatch, DivergenceError, SolveReport, UnsupportedOperator
 from .operator import GpuStencilOperator, as_operator, precond_scale
+from .precond import solve_tri, tri_spec, tri_inner_update
 
 INT_MAX = 2**31 - 1
 
@@ -303,6 +304,13 @@ def solve_stationary(A, f, schedule, P=None, tol=1e-6, max_outer=100_000, u0=Non
     if op.batch != 1:
         raise DimensionMismatch("use solve_stationary_batched for a batched operator")
     _check_len(op, f)
+    spec = tri_spec(P)
+    if spec is not None:         # Gauss-Seidel / SOR / SSOR (precond.py:79-118)
+        (u, rep), = solve_tri(op, f, schedule, *spec, tol=tol, max_outer=max_outer, u0=u0,
+                              check=check)
+        if isinstance(rep, DivergenceError):
+            raise rep
+        return u.reshape(-1), rep
     S = StationarySolver.cached(op, schedule, P, tol, max_outer, check, block_T)
     S.begin(f, u0)
     S.run()
@@ -330,10 +338,19 @@ def solve_stationary_batched(A, F, schedules, P=None, tol=1e-6, max_outer=100_00
         raise ValueError("check must be 'outer' or 'inner'")
     op = A if isinstance(A, GpuStencilOperator) else GpuStencilOperator.stack(
         [as_operator(a) for a in A])
-    S = StationarySolver.cached(op, schedules, P, tol, max_outer, check, block_T)
-    S.begin(F, u0)
-    S.run()
-    res = S.results(like_numpy=_is_host(F), out=out)
+    spec = tri_spec(P)
+    if spec is not None:
+        res = solve_tri(op, F, schedules, *spec, tol=tol, max_outer=max_outer, u0=u0,
+                        check=check)
+        if out is not None:
+            for b, (u, _) in enumerate(res):
+                if u is not None:
+                    out[b].copy_(torch.as_tensor(u).reshape(out[b].shape))
+    else:
+        S = StationarySolver.cached(op, schedules, P, tol, max_outer, check, block_T)
+        S.begin(F, u0)
+        S.run()
+        res = S.results(like_numpy=_is_host(F), out=out)
     if errors == "raise":
         for u, rep in res:
             if isinstance(rep, DivergenceError):
@@ -364,6 +381,8 @@ def _check_len(op, x):
 def inner_update(A, f, u, v, i, schedule, P=None):
     """One inner update (richardson.py:49-59); returns (u, v) like the inputs."""
     op = _op_for(A, f)
+    if tri_spec(P) is not None:
+        return tri_inner_update(op, f, u, v, i, schedule, tri_spec(P))
     ds = DeviceSchedule(op, schedule, P)
     host = _is_host(u)
     ut, vt, ft = op.to_device(u), op.to_device(v), op.to_device(f)
@@ -379,6 +398,8 @@ def outer_sweep(A, f, state, schedule, P=None):
     updates with the per-step finite check, then the residual norm appended
     to state.residual_history.  Mutates and returns `state`."""
     op = _op_for(A, f)
+    if tri_spec(P) is not None:
+        return _outer_sweep_tri(op, f, state, schedule, tri_spec(P))
     ds = DeviceSchedule(op, schedule, P)
     host = _is_host(state.u)
     u = op.to_device(state.u)
@@ -402,6 +423,27 @@ def outer_sweep(A, f, state, schedule, P=None):
     shp = np.shape(state.u) if host else state.u.shape
     state.u = _out(uf.reshape(shp), host)
     state.v = _out(vf.reshape(shp), host)
+    state.outer_count += 1
+    state.residual_history.append(float(np.sqrt(n2[0].item())) if op.batch == 1
+                                  else np.sqrt(n2.cpu().numpy()))
+    return state
+
+
+def _outer_sweep_tri(op, f, state, schedule, spec):
+    """outer_sweep (richardson.py:62-74) with a GS / SOR / SSOR map."""
+    host = _is_host(state.u)
+    shp = np.shape(state.u) if host else state.u.shape
+    u, v = op.to_device(state.u), op.to_device(state.v)
+    for i in range(len(np.atleast_1d(schedule.omega))):
+        u, v = tri_inner_update(op, f, u, v, i, schedule, spec)
+        if not (bool(torch.isfinite(u).all()) and bool(torch.isfinite(v).all())):
+            raise DivergenceError(
+                f"non-finite iterate in inner step {i + 1} of outer sweep "
+                f"{state.outer_count + 1}",
+                inner_iteration=state.outer_count * len(schedule.omega) + i + 1)
+    _, n2 = op.residual(u, op.to_device(f), want_r=False)
+    state.u = _out(u.reshape(shp), host)
+    state.v = _out(v.reshape(shp), host)
     state.outer_count += 1
     state.residual_history.append(float(np.sqrt(n2[0].item())) if op.batch == 1
                                   else np.sqrt(n2.cpu().numpy()))

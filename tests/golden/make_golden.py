@@ -278,7 +278,67 @@ def table2():
     save("table2", **out)
 
 
+def precond():
+    """GS / SOR / SSOR maps (precond.py:79-118) and SSOR-preconditioned
+    solves (the paper's NAGex + SSOR family) on small anisotropic grids."""
+    rng = np.random.default_rng(21)
+    out = {}
+    for k, n in enumerate((2, 9, 33)):
+        eps, th = float(10 ** rng.uniform(-3, 0)), float(rng.uniform(0, np.pi))
+        A = R.assemble_anisotropic(R.AnisotropicProblem(eps, th, n))
+        r = rng.standard_normal(A.ncols)
+        out.update({f"a{k}_n": n, f"a{k}_eps": eps, f"a{k}_theta": th, f"a{k}_r": r})
+        for name, P in (("gs", R.Preconditioner.gauss_seidel(A)),
+                        ("sor14", R.Preconditioner.sor(A, 1.4)),
+                        ("ssor10", R.Preconditioner.ssor(A, 1.0)),
+                        ("ssor13", R.Preconditioner.ssor(A, 1.3))):
+            out[f"a{k}_{name}"] = P.apply(r)
+    cases = (("ssor", 1.0, "plain", 4, 1e-8), ("ssor", 1.2, "nagex", 3, 1e-8),
+             ("gauss-seidel", 1.0, "mom", 2, 1e-8), ("sor", 1.5, "nag", 3, 1e-300),
+             ("ssor", 1.0, "plain", 1, 1e-8))
+    for k, (kind, relax, variant, m, tol) in enumerate(cases):
+        n = 24
+        eps, th = float(10 ** rng.uniform(-2, 0)), float(rng.uniform(0, np.pi))
+        A = R.assemble_anisotropic(R.AnisotropicProblem(eps, th, n))
+        f = rng.standard_normal(A.ncols)
+        P = {"ssor": lambda: R.Preconditioner.ssor(A, relax),
+             "sor": lambda: R.Preconditioner.sor(A, relax),
+             "gauss-seidel": lambda: R.Preconditioner.gauss_seidel(A)}[kind]()
+        BA = np.column_stack([P.apply(A.matvec(e)) for e in np.eye(A.ncols)])
+        lam = np.linalg.eigvals(BA)
+        lmax, lmin = float(lam.real.max()), float(lam.real.min())
+        if variant == "plain":
+            w = R.chebyshev_weights(lmax, lmin, m)
+            if k == 4:
+                w = np.array([4.0 / lmax])      # divergent on purpose
+        else:
+            w = np.linspace(0.8, 1.1, m) / lmax
+        kw = {} if variant == "plain" else {"alpha": np.linspace(0.2, 0.5, m)}
+        if variant == "nagex":
+            kw["alpha_tilde"] = np.linspace(0.6, 0.3, m)
+        sch = R.WeightSchedule(omega=w, variant=variant, **kw)
+        try:
+            u, rep = R.solve_stationary(A, f, sch, P=P, tol=tol, max_outer=60)
+            res = dict(u=u, trace=rep.trace, iterations=rep.iterations,
+                       inner=rep.inner_iterations, converged=rep.converged, diverged=-1)
+        except DivergenceError as e:
+            res = dict(u=np.zeros(0), trace=np.zeros(0), iterations=-1, inner=-1,
+                       converged=False, diverged=e.inner_iteration)
+        out.update({f"s{k}_{a}": b for a, b in res.items()})
+        out.update({f"s{k}_kind": kind, f"s{k}_relax": relax, f"s{k}_variant": variant,
+                    f"s{k}_n": n, f"s{k}_eps": eps, f"s{k}_theta": th, f"s{k}_f": f,
+                    f"s{k}_omega": sch.omega, f"s{k}_alpha": sch.alpha,
+                    f"s{k}_alpha_tilde": sch.alpha_tilde, f"s{k}_tol": tol})
+    out["n_apply"] = 3
+    out["n_solve"] = len(cases)
+    save("precond", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     cfg1()
     sweep_cases()
     edge_cases()

@@ -137,3 +137,39 @@ def test_oracle_matches_reference_fresh_draws(richlab):
         u, rep = R.solve_stationary(A, f, R.WeightSchedule(omega=w), tol=1e-7)
         uo, ro = O.solve_stationary(Ao, f, w, tol=1e-7)
         assert np.array_equal(u, uo) and rep.iterations == ro["iterations"]
+
+
+def _tri_from_golden(A, name):
+    return {"gs": ("gauss-seidel", 1.0), "sor14": ("sor", 1.4), "ssor10": ("ssor", 1.0),
+            "ssor13": ("ssor", 1.3)}[name]
+
+
+def test_tri_precond_apply(golden):
+    """GS / SOR / SSOR maps (precond.py:79-118) vs the reference's outputs."""
+    d = golden("precond")
+    for k in range(int(d["n_apply"])):
+        A = O.assemble_anisotropic(float(d[f"a{k}_eps"]), float(d[f"a{k}_theta"]),
+                                   int(d[f"a{k}_n"]))
+        for name in ("gs", "sor14", "ssor10", "ssor13"):
+            kind, relax = _tri_from_golden(A, name)
+            z = O.tri_precond(A, kind, relax)(d[f"a{k}_r"])
+            assert np.array_equal(z, d[f"a{k}_{name}"]), (k, name)
+
+
+def test_tri_precond_solves(golden):
+    """SSOR/SOR/GS-preconditioned solve_stationary vs the reference."""
+    d = golden("precond")
+    for k in range(int(d["n_solve"])):
+        g = lambda key: d[f"s{k}_{key}"]  # noqa: E731
+        A = O.assemble_anisotropic(float(g("eps")), float(g("theta")), int(g("n")))
+        pre = O.tri_precond(A, str(g("kind")), float(g("relax")))
+        try:
+            u, rep = O.solve_stationary(A, g("f"), g("omega"), g("alpha"), g("alpha_tilde"),
+                                        str(g("variant")), scale=pre, tol=float(g("tol")),
+                                        max_outer=60)
+        except O.OracleDivergence as e:
+            assert e.inner_iteration == int(g("diverged"))
+            continue
+        assert int(g("diverged")) == -1
+        assert np.array_equal(u, g("u")) and np.array_equal(rep["trace"], g("trace"))
+        assert rep["iterations"] == int(g("iterations")) and rep["inner_iterations"] == int(g("inner"))
