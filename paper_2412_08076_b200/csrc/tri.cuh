@@ -43,16 +43,22 @@ struct TriArgs {
 };
 
 // One substitution sweep: dst = oscale * x where M x = rhs, M lower
-// triangular in traversal order (reversed index order when rev).
-// rhs = src, or d * src when mul_d (SSOR's D * y).  Coefficients in
+// triangular in traversal order (reversed index order when REV).
+// rhs = src, or d * src when MULD (SSOR's D * y).  Coefficients in
 // traversal order: l0 (i-1, j-1), l1 (i-1, j), l2 (i-1, j+1), l3 (i, j-1).
-template <typename SI, typename SO>
-__device__ __forceinline__ void tri_sweep(const SI* src, SO* dst, int side, int P, bool rev,
-                                          bool mul_d, bool scale_out, double oscale, double l0,
-                                          double l1, double l2, double l3, double d, double* edge,
-                                          double (*xfer)[2]) {
+//
+// Every step ends in a block barrier, so the step time is the slowest
+// warp's body: the body is branch-free (predicated stores/loads, pointers
+// advanced per step) and warps whose rows have not started or are finished
+// skip whole windows of TRI_PF steps (barrier only).  x = t * (1/d): one rounding more than a
+// division, inside the 1e-13 bar.
+template <bool REV, bool MULD, bool SCALE, typename SI, typename SO>
+__device__ __forceinline__ void tri_sweep(const SI* __restrict__ src, SO* __restrict__ dst, int side,
+                                          int P, double oscale, double l0, double l1, double l2,
+                                          double l3, double d, double* edge, double (*xfer)[2]) {
     const int t = threadIdx.x, NT = blockDim.x, lane = t & 31, wp = t >> 5;
     const int nw = NT >> 5;
+    const double rd = 1.0 / d;
     for (int p0 = 0; p0 < side; p0 += NT) {
         const int ip = p0 + t;
         const bool row_ok = ip < side;
@@ -60,11 +66,15 @@ __device__ __forceinline__ void tri_sweep(const SI* src, SO* dst, int side, int 
         const int nsteps = side + 2 * (nrows - 1);
         if (t < nw) xfer[t][0] = xfer[t][1] = 0.0;
         __syncthreads();
-        const size_t rbase = (size_t)ip * side;
+        const long long rbase = (long long)ip * side;
+        // element jp of this thread's row (traversal order); clamped in-row
+        auto gptr = [&](int jp) -> long long {
+            const long long g = rbase + jp;
+            return REV ? (long long)P - 1 - g : g;
+        };
         auto ld = [&](int jp) -> double {
             if (!row_ok || jp < 0 || jp >= side) return 0.0;
-            const size_t g = rev ? (size_t)P - 1 - (rbase + jp) : rbase + jp;
-            return (double)src[g];
+            return (double)src[gptr(jp)];
         };
         double rq[TRI_PF];
 #pragma unroll
@@ -73,26 +83,43 @@ __device__ __forceinline__ void tri_sweep(const SI* src, SO* dst, int side, int 
         // thread 0 starts at column 0 with no warm-up steps: x(i-1, 0) of the
         // previous pass's last row seeds its window (zero for the first pass)
         if (t == 0 && p0 > 0) n0 = edge[0];
+        // warp's rows: lane 0 starts at step a0, lane 31 is done at a0 + 62 + side
+        const int a0 = 2 * 32 * wp;
         for (int s0 = 0; s0 < nsteps; s0 += TRI_PF) {
+            // idle before lane 0's warm-up step a0 - 1, and after lane 31
+            // relayed its trailing zero (step a0 + 62 + side)
+            const bool idle = (s0 + TRI_PF <= a0 - 1) || (s0 > a0 + 62 + side);
+            if (idle) {
+#pragma unroll
+                for (int q = 0; q < TRI_PF; ++q) {
+                    rq[q] = ld(s0 + TRI_PF + q - 2 * t);   // next window's rhs
+                    __syncthreads();
+                }
+                continue;
+            }
+            // one predicated body: pointers advance by one element per step
+            // whether or not the row is inside its column range
+            const int jp0 = s0 - 2 * t;
+            SO* out = dst + gptr(jp0);
+            const SI* in = src + gptr(jp0 + TRI_PF);
 #pragma unroll
             for (int q = 0; q < TRI_PF; ++q) {
                 const int s = s0 + q;
-                const int jp = s - 2 * t;
+                const int jp = jp0 + q;
+                const bool act = row_ok && (unsigned)jp < (unsigned)side;
                 double nb = __shfl_up_sync(0xffffffffu, pub, 1);
-                if (lane == 0) {
-                    if (wp > 0) nb = xfer[wp][(s + 1) & 1];
-                    else nb = (p0 > 0 && jp + 1 >= 0 && jp + 1 < side) ? edge[jp + 1] : 0.0;
-                }
-                double x = 0.0;
-                if (row_ok && jp >= 0 && jp < side) {
-                    double tt = mul_d ? d * rq[q] : rq[q];
-                    tt = tt - l0 * nm1;
-                    tt = tt - l1 * n0;
-                    tt = tt - l2 * nb;
-                    tt = tt - l3 * left;
-                    x = tt / d;
-                    const size_t g = rev ? (size_t)P - 1 - (rbase + jp) : rbase + jp;
-                    dst[g] = (SO)(scale_out ? oscale * x : x);
+                if (lane == 0)
+                    nb = wp > 0 ? xfer[wp][(s + 1) & 1]
+                                : ((p0 > 0 && (unsigned)(jp + 1) < (unsigned)side) ? edge[jp + 1]
+                                                                                  : 0.0);
+                double tt = MULD ? d * rq[q] : rq[q];
+                tt = tt - l0 * nm1;
+                tt = tt - l1 * n0;
+                tt = tt - l2 * nb;
+                tt = tt - l3 * left;
+                const double x = act ? tt * rd : 0.0;
+                if (act) {
+                    out[REV ? -q : q] = (SO)(SCALE ? oscale * x : x);
                     if (t == NT - 1) edge[jp] = x;
                 }
                 nm1 = n0;
@@ -100,7 +127,8 @@ __device__ __forceinline__ void tri_sweep(const SI* src, SO* dst, int side, int 
                 left = x;
                 pub = x;
                 if (lane == 31 && wp + 1 < nw) xfer[wp + 1][s & 1] = x;
-                rq[q] = ld(jp + TRI_PF);
+                const bool nact = row_ok && (unsigned)(jp + TRI_PF) < (unsigned)side;
+                rq[q] = nact ? (double)in[REV ? -q : q] : 0.0;
                 __syncthreads();
             }
         }
@@ -122,34 +150,37 @@ __global__ void __launch_bounds__(1024, 1) tri_kernel(const TriArgs<S> a) {
     const size_t base = (size_t)b * a.P;
     if (MODE == TRI_SOR) {
         // relax * solve(r)  (precond.py:93)
-        tri_sweep<S, S>(a.r + base, a.z + base, a.side, a.P, false, false, true, w, lo0, lo1, lo2,
-                        lo3, d, edge, xfer);
+        tri_sweep<false, false, true, S, S>(a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
+                                            lo3, d, edge, xfer);
     } else {
         // c * du(diag * dl(r))  (precond.py:109-110)
         const double cc = w * (2.0 - w);
-        tri_sweep<S, S>(a.r + base, a.work + base, a.side, a.P, false, false, false, 1.0, lo0, lo1,
-                        lo2, lo3, d, edge, xfer);
+        tri_sweep<false, false, false, S, S>(a.r + base, a.work + base, a.side, a.P, 1.0, lo0, lo1,
+                                             lo2, lo3, d, edge, xfer);
         __syncthreads();
-        tri_sweep<S, S>(a.work + base, a.z + base, a.side, a.P, true, true, true, cc, up0, up1, up2,
-                        up3, d, edge, xfer);
+        tri_sweep<true, true, true, S, S>(a.work + base, a.z + base, a.side, a.P, cc, up0, up1, up2,
+                                          up3, d, edge, xfer);
     }
+}
+
+template <typename S, int MODE>
+cudaError_t launch_tri_m(const TriArgs<S>& a, int batch, cudaStream_t st) {
+    int nt = (a.side + 31) / 32 * 32;
+    if (nt > 1024) nt = 1024;
+    const size_t smem = (size_t)a.side * sizeof(double);
+    auto k = tri_kernel<S, MODE>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<batch, nt, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 template <typename S>
 cudaError_t launch_tri(const TriArgs<S>& a, int mode, int batch, cudaStream_t st) {
-    int nt = ((a.side + 31) / 32) * 32;
-    if (nt > 1024) nt = 1024;
-    const size_t smem = (size_t)a.side * sizeof(double);
-    if (mode == TRI_SOR) {
-        auto k = tri_kernel<S, TRI_SOR>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<batch, nt, smem, st>>>(a);
-    } else {
-        auto k = tri_kernel<S, TRI_SSOR>;
-        if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        k<<<batch, nt, smem, st>>>(a);
-    }
-    return cudaGetLastError();
+    return mode == TRI_SOR ? launch_tri_m<S, TRI_SOR>(a, batch, st)
+                           : launch_tri_m<S, TRI_SSOR>(a, batch, st);
 }
 
 // Richardson update from an externally preconditioned residual z
