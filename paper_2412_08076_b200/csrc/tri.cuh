@@ -47,98 +47,149 @@ struct TriArgs {
 // rhs = src, or d * src when MULD (SSOR's D * y).  Coefficients in
 // traversal order: l0 (i-1, j-1), l1 (i-1, j), l2 (i-1, j+1), l3 (i, j-1).
 //
-// Every step ends in a block barrier, so the step time is the slowest
-// warp's body: the body is branch-free (predicated stores/loads, pointers
-// advanced per step) and warps whose rows have not started or are finished
-// skip whole windows of TRI_PF steps (barrier only).  x = t * (1/d): one rounding more than a
-// division, inside the 1e-13 bar.
+// Memory: at step s every thread touches a different grid row, so direct
+// loads/stores cost one L1 line per thread per step (measured ~340 ns per
+// wavefront step at 1023 rows).  Instead the steps run in windows of
+// TRI_PF: the rhs of window k+1 is fetched into shared memory with
+// cp.async while window k computes (each warp copies its own 32 rows, 8
+// lanes per row segment, coalesced), every step replaces its rhs slot with
+// the result, and the window is written back with coalesced stores.  The
+// step body itself touches only registers and shared memory.  Warps whose
+// rows have not started or are finished skip the compute (barriers only).
+// Arithmetic: x = rhs/d - (l0/d) nm1 - ... with FMAs (the kernel is
+// compiled without contraction; these are explicit): a different rounding
+// from SuperLU's, agreement ~1e-15, inside the reference's 1e-13 bar.
+constexpr int TRI_WS = TRI_PF + 1;   // padded row stride of the staging buffers
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async_el(void* sdst, const void* gsrc, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(sa), "l"(gsrc), "n"(BYTES),
+                 "r"(valid ? BYTES : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 template <bool REV, bool MULD, bool SCALE, typename SI, typename SO>
 __device__ __forceinline__ void tri_sweep(const SI* __restrict__ src, SO* __restrict__ dst, int side,
                                           int P, double oscale, double l0, double l1, double l2,
-                                          double l3, double d, double* edge, double (*xfer)[2]) {
+                                          double l3, double d, double* edge, double (*xfer)[2],
+                                          double* stage) {
+    static_assert(sizeof(SI) == 8 || sizeof(SI) == 4, "element size");
     const int t = threadIdx.x, NT = blockDim.x, lane = t & 31, wp = t >> 5;
     const int nw = NT >> 5;
     const double rd = 1.0 / d;
+    l0 *= rd;
+    l1 *= rd;
+    l2 *= rd;
+    l3 *= rd;
+    // staging: [2][NT][TRI_WS] doubles (f32 inputs are staged as raw 4-byte
+    // words in the low half of each slot and widened on use)
     for (int p0 = 0; p0 < side; p0 += NT) {
         const int ip = p0 + t;
         const bool row_ok = ip < side;
         const int nrows = min(NT, side - p0);
         const int nsteps = side + 2 * (nrows - 1);
+        const int nwin = (nsteps + TRI_PF - 1) / TRI_PF;
+        const int a0 = 2 * 32 * wp;   // lane 0 starts at a0; lane 31 done at a0 + 62 + side
         if (t < nw) xfer[t][0] = xfer[t][1] = 0.0;
-        __syncthreads();
-        const long long rbase = (long long)ip * side;
-        // element jp of this thread's row (traversal order); clamped in-row
-        auto gptr = [&](int jp) -> long long {
-            const long long g = rbase + jp;
+        auto gidx = [&](int row, int c) -> long long {   // row: index within the pass
+            const long long g = (long long)(p0 + row) * side + c;
             return REV ? (long long)P - 1 - g : g;
         };
-        auto ld = [&](int jp) -> double {
-            if (!row_ok || jp < 0 || jp >= side) return 0.0;
-            return (double)src[gptr(jp)];
+        auto idle_win = [&](int k) {
+            const int s0 = k * TRI_PF;
+            return (s0 + TRI_PF <= a0 - 1) || (s0 > a0 + 62 + side);
         };
-        double rq[TRI_PF];
+        // warp-cooperative window copies: lane -> (row 32 wp + lane/8 + 4 it, slot lane%8)
+        auto load_win = [&](int k) {
+            double* b = stage + (size_t)(k & 1) * NT * TRI_WS;
 #pragma unroll
-        for (int q = 0; q < TRI_PF; ++q) rq[q] = ld(q - 2 * t);
+            for (int it = 0; it < 8; ++it) {
+                const int row = wp * 32 + (lane >> 3) + 4 * it;
+                const int c = k * TRI_PF + (lane & 7) - 2 * row;
+                const bool ok = p0 + row < side && c >= 0 && c < side;
+                cp_async_el<sizeof(SI)>(&b[row * TRI_WS + (lane & 7)], src + (ok ? gidx(row, c) : 0), ok);
+            }
+            cp_async_commit();
+        };
+        auto store_win = [&](int k) {
+            const double* b = stage + (size_t)(k & 1) * NT * TRI_WS;
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const int row = wp * 32 + (lane >> 3) + 4 * it;
+                const int c = k * TRI_PF + (lane & 7) - 2 * row;
+                if (p0 + row < side && c >= 0 && c < side)
+                    dst[gidx(row, c)] = (SO)b[row * TRI_WS + (lane & 7)];
+            }
+        };
+        auto rhs_at = [&](const double* slot) -> double {
+            if (sizeof(SI) == 8) return *slot;
+            return (double)*reinterpret_cast<const float*>(slot);
+        };
+        if (!idle_win(0)) load_win(0);
         double left = 0.0, nm1 = 0.0, n0 = 0.0, pub = 0.0;
         // thread 0 starts at column 0 with no warm-up steps: x(i-1, 0) of the
         // previous pass's last row seeds its window (zero for the first pass)
         if (t == 0 && p0 > 0) n0 = edge[0];
-        // warp's rows: lane 0 starts at step a0, lane 31 is done at a0 + 62 + side
-        const int a0 = 2 * 32 * wp;
-        for (int s0 = 0; s0 < nsteps; s0 += TRI_PF) {
-            // idle before lane 0's warm-up step a0 - 1, and after lane 31
-            // relayed its trailing zero (step a0 + 62 + side)
-            const bool idle = (s0 + TRI_PF <= a0 - 1) || (s0 > a0 + 62 + side);
+        for (int k = 0; k < nwin; ++k) {
+            const bool idle = idle_win(k);
+            cp_async_wait_all();          // window k's rhs (issued one window ago)
+            __syncwarp();
+            if (k + 1 < nwin && !idle_win(k + 1)) load_win(k + 1);
+            __syncthreads();
             if (idle) {
 #pragma unroll
-                for (int q = 0; q < TRI_PF; ++q) {
-                    rq[q] = ld(s0 + TRI_PF + q - 2 * t);   // next window's rhs
-                    __syncthreads();
-                }
+                for (int q = 0; q < TRI_PF - 1; ++q) __syncthreads();
                 continue;
             }
-            // one predicated body: pointers advance by one element per step
-            // whether or not the row is inside its column range
-            const int jp0 = s0 - 2 * t;
-            SO* out = dst + gptr(jp0);
-            const SI* in = src + gptr(jp0 + TRI_PF);
+            double* b = stage + ((size_t)(k & 1) * NT + t) * TRI_WS;
+            const int s0 = k * TRI_PF;
 #pragma unroll
             for (int q = 0; q < TRI_PF; ++q) {
                 const int s = s0 + q;
-                const int jp = jp0 + q;
+                const int jp = s - 2 * t;
                 const bool act = row_ok && (unsigned)jp < (unsigned)side;
-                double nb = __shfl_up_sync(0xffffffffu, pub, 1);
-                if (lane == 0)
-                    nb = wp > 0 ? xfer[wp][(s + 1) & 1]
-                                : ((p0 > 0 && (unsigned)(jp + 1) < (unsigned)side) ? edge[jp + 1]
-                                                                                  : 0.0);
-                double tt = MULD ? d * rq[q] : rq[q];
-                tt = tt - l0 * nm1;
-                tt = tt - l1 * n0;
-                tt = tt - l2 * nb;
-                tt = tt - l3 * left;
-                const double x = act ? tt * rd : 0.0;
-                if (act) {
-                    out[REV ? -q : q] = (SO)(SCALE ? oscale * x : x);
-                    if (t == NT - 1) edge[jp] = x;
-                }
+                // x(i-1, j+1): lane - 1 (shuffle), the previous warp's lane 31
+                // (mailbox) or the previous pass's last row (edge); selects
+                // instead of a divergent branch
+                const double sh = __shfl_up_sync(0xffffffffu, pub, 1);
+                const double mb = xfer[wp][(s + 1) & 1];
+                const int ce = min(max(jp + 1, 0), side - 1);
+                const double ev = (p0 > 0 && (unsigned)(jp + 1) < (unsigned)side) ? edge[ce] : 0.0;
+                const double nb = lane != 0 ? sh : (wp > 0 ? mb : ev);
+                // x = (rhs - l0 nm1 - l1 n0 - l2 nb - l3 left) / d, as
+                // rhs/d - (l/d) x with FMAs: two dependent FMAs per step
+                // after the neighbour value arrives
+                const double rv = rhs_at(&b[q]);
+                double u = MULD ? rv : rv * rd;          // (d y) / d = y for SSOR's D y
+                u = __fma_rn(-l0, nm1, u);
+                u = __fma_rn(-l1, n0, u);
+                u = __fma_rn(-l2, nb, u);
+                const double x = act ? __fma_rn(-l3, left, u) : 0.0;
+                b[q] = SCALE ? oscale * x : x;
+                if (act && t == NT - 1) edge[jp] = x;
                 nm1 = n0;
                 n0 = nb;
                 left = x;
                 pub = x;
                 if (lane == 31 && wp + 1 < nw) xfer[wp + 1][s & 1] = x;
-                const bool nact = row_ok && (unsigned)(jp + TRI_PF) < (unsigned)side;
-                rq[q] = nact ? (double)in[REV ? -q : q] : 0.0;
-                __syncthreads();
+                if (q + 1 < TRI_PF) __syncthreads();
             }
+            __syncwarp();
+            store_win(k);
         }
+        cp_async_wait_all();
         __syncthreads();
     }
 }
 
 template <typename S, int MODE>
 __global__ void __launch_bounds__(1024, 1) tri_kernel(const TriArgs<S> a) {
-    extern __shared__ double edge[];
+    extern __shared__ double tri_smem[];
+    double* stage = tri_smem;                                        // [2][NT][TRI_WS]
+    double* edge = tri_smem + 2 * (size_t)blockDim.x * TRI_WS;        // [side]
     __shared__ double xfer[32][2];
     const int b = blockIdx.x;
     const double* c = a.stencil + (size_t)(a.shared ? 0 : b) * 9;
@@ -151,15 +202,15 @@ __global__ void __launch_bounds__(1024, 1) tri_kernel(const TriArgs<S> a) {
     if (MODE == TRI_SOR) {
         // relax * solve(r)  (precond.py:93)
         tri_sweep<false, false, true, S, S>(a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
-                                            lo3, d, edge, xfer);
+                                            lo3, d, edge, xfer, stage);
     } else {
         // c * du(diag * dl(r))  (precond.py:109-110)
         const double cc = w * (2.0 - w);
         tri_sweep<false, false, false, S, S>(a.r + base, a.work + base, a.side, a.P, 1.0, lo0, lo1,
-                                             lo2, lo3, d, edge, xfer);
+                                             lo2, lo3, d, edge, xfer, stage);
         __syncthreads();
         tri_sweep<true, true, true, S, S>(a.work + base, a.z + base, a.side, a.P, cc, up0, up1, up2,
-                                          up3, d, edge, xfer);
+                                          up3, d, edge, xfer, stage);
     }
 }
 
@@ -167,9 +218,9 @@ template <typename S, int MODE>
 cudaError_t launch_tri_m(const TriArgs<S>& a, int batch, cudaStream_t st) {
     int nt = (a.side + 31) / 32 * 32;
     if (nt > 1024) nt = 1024;
-    const size_t smem = (size_t)a.side * sizeof(double);
+    const size_t smem = (2 * (size_t)nt * TRI_WS + a.side) * sizeof(double);
     auto k = tri_kernel<S, MODE>;
-    if (smem > 48 * 1024) {
+    {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }

@@ -7,7 +7,6 @@ NAGex(3) + SSOR family), and the oracle's (SuperLU) time for one application.
 """
 import argparse
 import json
-import os
 import sys
 import time
 from pathlib import Path
@@ -48,16 +47,10 @@ def main():
         for kind, relax in (("sor", 1.5), ("ssor", 1.0)):
             pre = G.TriangularPreconditioner(op, kind, relax)
             passes = 1 if kind == "sor" else 2
-            for rpt in ("1", "2", "4", None):
-                if rpt is None:
-                    os.environ.pop("RG_TRI_R", None)
-                else:
-                    os.environ["RG_TRI_R"] = rpt
-                ms = ev_time(lambda: pre.apply_device(R, Z, W), 5)
-                row[f"{kind}_R{rpt or 'auto'}"] = {
-                    "ms_per_apply_batch": ms, "systems": B,
-                    "point_solves_per_s": passes * B * op.P / (ms * 1e-3),
-                    "ns_per_wavefront_step": ms * 1e6 / (passes * (3 * (n - 1) - 2))}
+            ms = ev_time(lambda: pre.apply_device(R, Z, W), 5)
+            row[kind] = {"ms_per_apply_batch": ms, "systems": B,
+                         "point_solves_per_s": passes * B * op.P / (ms * 1e-3),
+                         "ns_per_wavefront_step": ms * 1e6 / (passes * (3 * (n - 1) - 2))}
         if not args.no_cpu:
             f = O.tri_precond(As[0], "ssor", 1.0)
             r0 = R[0].cpu().numpy()
