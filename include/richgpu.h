@@ -205,6 +205,25 @@ int rg_tri_apply(const rg_op* A, int kind, double relax, const void* r, void* z,
 int rg_precond_update(const rg_op* A, const rg_sched* s, int i, const void* z,
                       void* u, void* v, void* y, void* stream);
 
+/* ---- training unroll adjoint (training.py:84-104, tape.py:191-199) --------
+ * Reverse pass of the K-step unroll from u_0 = v_0 = 0 whose loss is
+ * L = ||f - A u_K|| / ||f|| (float64, CONST9 or VAR9; At = the operator
+ * holding A^T, equal to A for the symmetric anisotropic stencils).  The
+ * forward histories u_k, v_k come from rg_inner_update.
+ * init: loss[b] = L_b, ubar = dL/du_K, vbar = 0 (rwork: [batch][P] scratch).
+ * step (k = K-1 .. 0, i = k mod m): ubar/vbar go from the adjoints of
+ * u_{k+1}, v_{k+1} to those of u_k, v_k in place, and dots[3][batch] gets
+ * the contributions of step k to dL/dalpha_i, dL/domega_i and
+ * dL/dalpha_tilde_i (the last zero for plain/mom).  Jacobi (scalar/field)
+ * or no preconditioner.  Deterministic fixed-order reductions. */
+int rg_unroll_adjoint_init(const rg_op* A, const rg_op* At, const void* uK,
+                           const void* f, void* rwork, void* ubar, void* vbar,
+                           double* loss, void* stream);
+int rg_unroll_adjoint_step(const rg_op* A, const rg_op* At, const rg_sched* s,
+                           int i, const void* f, const void* u_k, const void* v_k,
+                           void* ubar, void* vbar, void* rbar, double* dots,
+                           void* stream);
+
 /* ---- solve_stationary engine (richardson.py:77-141) ----------------------
  * A solver owns device workspace (per-system status, trace, reduction
  * partials) and runs the whole loop on the device: convergence, divergence

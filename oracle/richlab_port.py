@@ -419,4 +419,58 @@ def fgmres(A, f, precond, restart=20, tol=1e-6, max_outer=100):
                    trace=np.array(trace), stagnated=stagnated)
 
 
+
+
+# ----------------------------------------------------------- training.py (unroll)
+def unroll_forward(A, f, omega, alpha, alpha_t, K, variant, scale=None):
+    """training.py:61-81: K inner updates from u = v = 0; returns (loss,
+    histories us, vs, ps) with p_k = P r_k."""
+    n = A.shape[1]
+    u, v = np.zeros(n), np.zeros(n)
+    us, vs, ps = [u], [v], []
+    m = len(omega)
+    for k in range(K):
+        i = k % m
+        y = u if variant in ("plain", "mom") else u + alpha_t[i] * v
+        r = f - A.dot(y)
+        p = _precond(scale, r)
+        v = (alpha[i] * v + omega[i] * p) if variant != "plain" else omega[i] * p
+        u = u + v
+        us.append(u)
+        vs.append(v)
+        ps.append(p)
+    return float(np.linalg.norm(f - A.dot(u)) / np.linalg.norm(f)), us, vs, ps
+
+
+def unroll_grad(A, f, omega, alpha, alpha_t, K, variant, scale=None):
+    """Reverse pass of _unroll_tape (training.py:84-104) as the tape performs
+    it (tape.py:28-42, vjps of tape.py:93-133,191-199): returns (loss,
+    d_omega, d_alpha, d_alpha_t).  `scale`: Jacobi scale (P^T = P)."""
+    m = len(omega)
+    loss, us, vs, ps = unroll_forward(A, f, omega, alpha, alpha_t, K, variant, scale)
+    fnorm = float(np.linalg.norm(f))
+    r = f - A.dot(us[K])
+    nr = np.linalg.norm(r)
+    g = (1.0 / fnorm) * (r / nr)
+    ubar = -(A.T.dot(g))
+    vbar = np.zeros_like(ubar)
+    dw, da, dat = np.zeros(m), np.zeros(m), np.zeros(m)
+    nag = variant in ("nag", "nagex")
+    for k in range(K - 1, -1, -1):
+        i = k % m
+        vt = vbar + ubar
+        if variant != "plain":
+            da[i] += np.sum(vt * vs[k])
+        dw[i] += np.sum(vt * ps[k])
+        pbar = omega[i] * vt
+        rbar = pbar if scale is None else scale * pbar
+        ybar = -(A.T.dot(rbar))
+        ubar = ubar + ybar
+        vbar = alpha[i] * vt if variant != "plain" else np.zeros_like(vt)
+        if nag:
+            vbar = vbar + alpha_t[i] * ybar
+            dat[i] += np.sum(ybar * vs[k])
+    return loss, dw, da, dat
+
+
 __all__ = [n for n in dir() if not n.startswith("_")]

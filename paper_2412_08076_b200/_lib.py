@@ -54,6 +54,9 @@ _SIGS = [
     ("rg_residual", _I, [_P, _P, _P, _P, _P, _P]),
     ("rg_inner_update", _I, [_P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P, _P, _I, _P]),
     ("rg_tri_apply", _I, [_P, _I, C.c_double, _P, _P, _P, _P]),
+    ("rg_unroll_adjoint_init", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    ("rg_unroll_adjoint_step", _I, [_P, _P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P, _P, _P,
+                                    _P]),
     ("rg_precond_update", _I, [_P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P]),
     ("rg_sweep", _I, [_P, C.POINTER(rg_sched), _I, _I, _I, _P, _P, _P, _P, _P, C.POINTER(_I), _P]),
     ("rg_dst_create", _I, [C.POINTER(_P), _I, _I]),

@@ -17,8 +17,10 @@
 #include "mg.cuh"
 #include "cluster.cuh"
 #include "krylov.cuh"
+#include <type_traits>
 #include "cblock.cuh"
 #include "tri.cuh"
+#include "adjoint.cuh"
 
 using namespace rg;
 
@@ -340,6 +342,14 @@ static int chunk_len(int n, int T, int i) {
 }
 
 // ==================================================================== C ABI
+// CONST9 / VAR9 dispatch for the adjoint kernels
+template <typename K>
+static cudaError_t by_kind(int kind, K k) {
+    if (kind == RG_CONST9) k(std::integral_constant<int, K_CONST9>());
+    else k(std::integral_constant<int, K_VAR9>());
+    return cudaGetLastError();
+}
+
 extern "C" {
 
 int rg_version(void) { return RG_ABI_VERSION; }
@@ -539,6 +549,87 @@ int rg_precond_update(const rg_op* A, const rg_sched* s, int i, const void* z, v
     }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? RG_OK : fail(RG_ECUDA, "update launch: %s", cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------- adjoint
+static int check_adj_ops(const rg_op* A, const rg_op* At) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if ((rc = check_op(At))) return rc;
+    if (A->d.dtype != RG_F64 || At->d.dtype != RG_F64)
+        return fail(RG_EUNSUPPORTED, "the unroll adjoint runs on float64 operators");
+    if (A->d.kind != At->d.kind || (A->d.kind != RG_CONST9 && A->d.kind != RG_VAR9))
+        return fail(RG_EUNSUPPORTED, "the unroll adjoint needs CONST9 or VAR9 operators A, A^T");
+    if (A->d.side != At->d.side || A->d.batch != At->d.batch)
+        return fail(RG_ESIZE, "A and A^T disagree in side or batch");
+    return RG_OK;
+}
+
+int rg_unroll_adjoint_init(const rg_op* A, const rg_op* At, const void* uK, const void* f,
+                           void* rwork, void* ubar, void* vbar, double* loss, void* stream) {
+    int rc = check_adj_ops(A, At);
+    if (rc) return rc;
+    if (!uK || !f || !rwork || !ubar || !vbar || !loss) return fail(RG_ENULL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const dim3 g = step_grid(A), blk(STEP_BX, STEP_BY);
+    const int ncta = g.x * g.y, B = A->d.batch;
+    double *part = nullptr, *sums = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double) * 2 * B * ncta, st));
+    CUDA_TRY(cudaMallocAsync((void**)&sums, sizeof(double) * 2 * B, st));
+    const OpView<double> av = view<double>(A), tv = view<double>(At);
+    cudaError_t e = by_kind(A->d.kind, [&](auto kk) {
+        constexpr int KIND = decltype(kk)::value;
+        adj_seed_a_kernel<KIND><<<g, blk, 0, st>>>(av, (const double*)uK, (const double*)f,
+                                                   (double*)rwork, part);
+        sum_partials_kernel<256><<<2 * B, 256, 0, st>>>(part, ncta, sums);
+        adj_seed_scale_kernel<<<dim3(64, B), 256, 0, st>>>(B, A->P, sums, (double*)rwork, loss);
+        adj_seed_b_kernel<KIND><<<g, blk, 0, st>>>(tv, (const double*)rwork, (double*)ubar,
+                                                   (double*)vbar);
+    });
+    if (e != cudaSuccess) rc = fail(RG_ECUDA, "adjoint seed launch: %s", cudaGetErrorString(e));
+    CUDA_TRY(cudaFreeAsync(part, st));
+    CUDA_TRY(cudaFreeAsync(sums, st));
+    return rc;
+}
+
+int rg_unroll_adjoint_step(const rg_op* A, const rg_op* At, const rg_sched* s, int i,
+                           const void* f, const void* u_k, const void* v_k, void* ubar,
+                           void* vbar, void* rbar, double* dots, void* stream) {
+    int rc = check_adj_ops(A, At);
+    if (rc) return rc;
+    if ((rc = check_sched(A, s))) return rc;
+    if (i < 0 || i >= s->m) return fail(RG_EINVAL, "inner index %d outside [0, %d)", i, s->m);
+    if (!f || !u_k || !v_k || !ubar || !vbar || !rbar || !dots) return fail(RG_ENULL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const dim3 g = step_grid(A), blk(STEP_BX, STEP_BY);
+    const int ncta = g.x * g.y, B = A->d.batch;
+    AdjArgs a;
+    a.A = view<double>(A);
+    a.At = view<double>(At);
+    a.f = (const double*)f;
+    a.u = (const double*)u_k;
+    a.v = (const double*)v_k;
+    a.ubar = (double*)ubar;
+    a.vbar = (double*)vbar;
+    a.rbar = (double*)rbar;
+    a.omega = s->omega;
+    a.alpha = s->variant == RG_PLAIN ? nullptr : s->alpha;
+    a.atil = s->alpha_tilde;
+    a.scale = (const double*)s->scale;
+    a.precond = s->precond;
+    a.m = s->m;
+    a.i = i;
+    a.nag = s->variant >= RG_NAG;
+    CUDA_TRY(cudaMallocAsync((void**)&a.part, sizeof(double) * 3 * B * ncta, st));
+    cudaError_t e = by_kind(A->d.kind, [&](auto kk) {
+        constexpr int KIND = decltype(kk)::value;
+        adj_a_kernel<KIND><<<g, blk, 0, st>>>(a);
+        adj_b_kernel<KIND><<<g, blk, 0, st>>>(a);
+        sum_partials_kernel<256><<<3 * B, 256, 0, st>>>(a.part, ncta, dots);
+    });
+    if (e != cudaSuccess) rc = fail(RG_ECUDA, "adjoint step launch: %s", cudaGetErrorString(e));
+    CUDA_TRY(cudaFreeAsync(a.part, st));
+    return rc;
 }
 
 int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,

@@ -334,6 +334,46 @@ def precond():
     save("precond", **out)
 
 
+def unroll():
+    """Training unroll (training.py:61-104): the tape-free loss and the tape
+    gradients of _unroll_tape w.r.t. omega / alpha / alpha_t (separate Vars)."""
+    from richlab import training as RT
+    from richlab.tape import Tape
+    rng = np.random.default_rng(31)
+    out = {}
+    cases = [("plain", None), ("mom", None), ("nag", None), ("nagex", None),
+             ("plain", "jacobi"), ("nag", "jacobi"), ("mom", "jacobi")]
+    for k, (variant, pre) in enumerate(cases):
+        n = int(rng.choice([12, 17]))
+        eps, th = float(10 ** rng.uniform(-2, 0)), float(rng.uniform(0, np.pi))
+        A = R.assemble_anisotropic(R.AnisotropicProblem(eps, th, n))
+        f = rng.standard_normal(A.ncols)
+        m, K = 3, 11
+        P = R.Preconditioner.weighted_jacobi(A) if pre == "jacobi" else None
+        lam = np.linalg.eigvalsh(A.to_dense()).max()
+        scale = (2.0 / 3.0) / A.diagonal()[0] if pre == "jacobi" else 1.0
+        w = rng.uniform(0.3, 0.9, m) / (lam * scale)
+        a = rng.uniform(0.1, 0.5, m)
+        at = rng.uniform(0.1, 0.5, m) if variant == "nagex" else a.copy()
+        tape = Tape()
+        om = tape.var(w)
+        al = tape.var(a) if variant != "plain" else None
+        atv = tape.var(at)
+        loss = RT._unroll_tape(A, f, om, al, atv, K, variant, P)
+        tape.backward(loss)
+        free = RT.unrolled_relative_residual(A, f, w, a if variant != "plain" else np.zeros(m),
+                                             at, K, variant, P)
+        out.update({f"u{k}_variant": variant, f"u{k}_pre": pre or "none", f"u{k}_n": n,
+                    f"u{k}_eps": eps, f"u{k}_theta": th, f"u{k}_f": f, f"u{k}_K": K,
+                    f"u{k}_omega": w, f"u{k}_alpha": a, f"u{k}_alpha_t": at,
+                    f"u{k}_loss": float(loss.value), f"u{k}_loss_free": free,
+                    f"u{k}_d_omega": om.grad,
+                    f"u{k}_d_alpha": al.grad if al is not None else np.zeros(m),
+                    f"u{k}_d_alpha_t": atv.grad if atv.grad is not None else np.zeros(m)})
+    out["count"] = len(cases)
+    save("unroll", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
@@ -346,3 +386,5 @@ if __name__ == "__main__":
     fns_dst()
     multigrid()
     table2()
+    precond()
+    unroll()

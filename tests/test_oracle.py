@@ -173,3 +173,17 @@ def test_tri_precond_solves(golden):
         assert int(g("diverged")) == -1
         assert np.array_equal(u, g("u")) and np.array_equal(rep["trace"], g("trace"))
         assert rep["iterations"] == int(g("iterations")) and rep["inner_iterations"] == int(g("inner"))
+
+
+def test_unroll_grad_vs_reference_tape(golden):
+    """Training unroll (training.py:61-104): loss and tape gradients."""
+    d = golden("unroll")
+    for k in range(int(d["count"])):
+        g = lambda key: d[f"u{k}_{key}"]  # noqa: E731
+        A = O.assemble_anisotropic(float(g("eps")), float(g("theta")), int(g("n")))
+        sc = O.jacobi_scale(A) if str(g("pre")) == "jacobi" else None
+        loss, dw, da, dat = O.unroll_grad(A, g("f"), g("omega"), g("alpha"), g("alpha_t"),
+                                          int(g("K")), str(g("variant")), sc)
+        assert loss == float(g("loss_free"))
+        for got, want in ((dw, g("d_omega")), (da, g("d_alpha")), (dat, g("d_alpha_t"))):
+            assert np.allclose(got, want, rtol=1e-12, atol=1e-15), (k, got, want)
