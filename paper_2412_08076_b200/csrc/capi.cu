@@ -350,6 +350,22 @@ static cudaError_t by_kind(int kind, K k) {
     return cudaGetLastError();
 }
 
+// Stream-ordered scratch (reduction partials) comes from the device's
+// default memory pool.  Its default release threshold (0) hands memory back
+// to the driver at every synchronisation, which made the first allocation
+// after each host sync cost ~0.9 ms (measured in the FGMRES loop); keep it.
+static void ensure_pool() {
+    static bool done[64] = {false};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 extern "C" {
 
 int rg_version(void) { return RG_ABI_VERSION; }
@@ -449,6 +465,7 @@ int rg_residual(const rg_op* A, const void* u, const void* f, void* r, double* n
     const dim3 g = step_grid(A);
     const int ncta = g.x * g.y;
     if (norm2) {
+        ensure_pool();
         CUDA_TRY(cudaMallocAsync((void**)&q.partials, sizeof(double) * ncta * A->d.batch, st));
     }
     rc = step1(A, q, st);
@@ -574,7 +591,9 @@ int rg_unroll_adjoint_init(const rg_op* A, const rg_op* At, const void* uK, cons
     const dim3 g = step_grid(A), blk(STEP_BX, STEP_BY);
     const int ncta = g.x * g.y, B = A->d.batch;
     double *part = nullptr, *sums = nullptr;
+    ensure_pool();
     CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double) * 2 * B * ncta, st));
+    ensure_pool();
     CUDA_TRY(cudaMallocAsync((void**)&sums, sizeof(double) * 2 * B, st));
     const OpView<double> av = view<double>(A), tv = view<double>(At);
     cudaError_t e = by_kind(A->d.kind, [&](auto kk) {
@@ -620,6 +639,7 @@ int rg_unroll_adjoint_step(const rg_op* A, const rg_op* At, const rg_sched* s, i
     a.m = s->m;
     a.i = i;
     a.nag = s->variant >= RG_NAG;
+    ensure_pool();
     CUDA_TRY(cudaMallocAsync((void**)&a.part, sizeof(double) * 3 * B * ncta, st));
     cudaError_t e = by_kind(A->d.kind, [&](auto kk) {
         constexpr int KIND = decltype(kk)::value;
@@ -845,6 +865,7 @@ int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void*
     int ncta = (n + MGS_NT * 4 - 1) / (MGS_NT * 4);
     if (ncta > 512) ncta = 512;
     double* part = nullptr;
+    ensure_pool();
     CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double) * 3 * ncta * batch, st));
     const dim3 g(ncta, batch);
     if (dtype == RG_F64) {

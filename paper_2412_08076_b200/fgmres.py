@@ -151,11 +151,13 @@ def fgmres_batched(A, F, precond_apply=None, cfg: FgmresConfig = None, U0=None):
                     hs.append(h)
                 hk1 = torch.linalg.vector_norm(w, dim=1)
                 H = torch.stack(hs, dim=1)                     # [G, k+1]
+            # one device->host copy per group: [G, k+2] = (h_0..h_k, ||w||)
+            Hh = torch.cat([H, hk1.to(H.dtype)[:, None]], dim=1).cpu().numpy()
             for q, b in enumerate(bs):
-                hcols[b] = H[q]
-                hk1s[b] = hk1[q]
+                hcols[b] = Hh[q, :k + 1]
+                hk1s[b] = float(np.real(Hh[q, k + 1]))
                 systems[b]._w = w[q]
-        hcol_h = {b: (hcols[b].cpu().numpy(), float(hk1s[b].item())) for b in hcols}
+        hcol_h = {b: (hcols[b], hk1s[b]) for b in hcols}
         for s in run:
             hc, hk1 = hcol_h[s.b]
             k, H, cs, sn, g = s.k, s.H, s.cs, s.sn, s.g

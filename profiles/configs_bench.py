@@ -200,6 +200,9 @@ def run_cfg5():
     h.apply(Fd)
     tv = cuda_time(lambda: h.apply(Fd), reps=3)
     cfg = GG.FgmresConfig(restart=c["restart"], tol=1e-6, max_outer=c["max_outer"])
+    # warm-up (module loading, pool growth) with a 2-step FGMRES
+    GG.fgmres_batched(op, Fd, precond_apply=lambda R: h.apply(R),
+                      cfg=GG.FgmresConfig(restart=2, tol=1e-6, max_outer=1))
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = GG.fgmres_batched(op, Fd, precond_apply=lambda R: h.apply(R), cfg=cfg)

@@ -34,6 +34,8 @@ def timed(name, fn):
 
 
 h.apply(Fd)
+GG.fgmres_batched(op, Fd, precond_apply=lambda R: h.apply(R),
+                  cfg=GG.FgmresConfig(restart=2, tol=1e-6, max_outer=1))   # warm-up
 orig_mv = GG._matvec
 GG._matvec = timed("matvec", orig_mv)
 torch.cuda.synchronize()
