@@ -58,6 +58,17 @@ struct rg_op {
     std::vector<double> hcoef;   // CONST9 real: host copy of [batch][9] (kernel params)
     bool cblock_ok = false;      // DIAG5 c128 with one set of off-diagonals: blocked sweep
     double2 hoff[4];
+    // VAR9 c128 whose rows mostly repeat one stencil (Galerkin levels of the
+    // sponge Helmholtz operator: ~96% of rows bit-identical to the centre
+    // row): that stencil as kernel parameters + a per-node "row == stencil"
+    // flag, so the blocked sweep reads coefficient planes only in the band
+    // where they vary.
+    bool var9h = false;
+    double2 hc9[9];
+    unsigned char* mask = nullptr;  // device [P] (owned)
+    ~rg_op() {
+        if (mask) cudaFree(mask);
+    }
 };
 
 struct rg_solver {
@@ -341,6 +352,19 @@ static int chunk_len(int n, int T, int i) {
     return 1;
 }
 
+// balanced chunks of at most T steps (the complex blocked sweeps instantiate T <= 4)
+static int chunk_cap(int n, int T, int i) {
+    const int nc = (n + T - 1) / T;
+    const int base = n / nc, rem = n % nc;
+    int start = 0;
+    for (int c = 0; c < nc; ++c) {
+        const int len = base + (c < rem ? 1 : 0);
+        if (i < start + len) return start + len - i;
+        start += len;
+    }
+    return 1;
+}
+
 // ==================================================================== C ABI
 // CONST9 / VAR9 dispatch for the adjoint kernels
 template <typename K>
@@ -413,6 +437,44 @@ int rg_op_create(rg_op** out, const rg_op_desc* d) {
                     same = same && off[b * 4 + q].x == off[q].x && off[b * 4 + q].y == off[q].y;
             A->cblock_ok = same;
             for (int q = 0; q < 4; ++q) A->hoff[q] = off[q];
+        }
+    }
+    if (d->kind == RG_VAR9 && d->dtype == RG_C128 && (d->shared || d->batch == 1)) {
+        // one coefficient set: find the rows equal (on their in-grid entries)
+        // to the centre row; worth it when they are the large majority
+        const int side = d->side;
+        const size_t P = A->P;
+        std::vector<double2> pl(9 * P);
+        if (cudaMemcpy(pl.data(), d->stencil, pl.size() * sizeof(double2), cudaMemcpyDeviceToHost) ==
+                cudaSuccess && side >= 3) {
+            const size_t ic = (size_t)(side / 2) * side + side / 2;
+            double2 c[9];
+            for (int q = 0; q < 9; ++q) c[q] = pl[q * P + ic];
+            std::vector<unsigned char> m(P);
+            size_t same = 0;
+            for (int i = 0; i < side; ++i)
+                for (int j = 0; j < side; ++j) {
+                    const size_t idx = (size_t)i * side + j;
+                    bool eq = true;
+                    for (int q = 0; q < 9 && eq; ++q) {
+                        const int ii = i + q / 3 - 1, jj = j + q % 3 - 1;
+                        if (ii < 0 || ii >= side || jj < 0 || jj >= side) continue;   // zero-padded
+                        const double2 v = pl[q * P + idx];
+                        // bitwise equality (distinguishes +0 / -0)
+                        eq = memcmp(&v, &c[q], sizeof(double2)) == 0;
+                    }
+                    m[idx] = eq ? 1 : 0;
+                    same += eq;
+                }
+            if (same * 4 >= P * 3 && cudaMalloc((void**)&A->mask, P) == cudaSuccess) {
+                if (cudaMemcpy(A->mask, m.data(), P, cudaMemcpyHostToDevice) == cudaSuccess) {
+                    A->var9h = true;
+                    for (int q = 0; q < 9; ++q) A->hc9[q] = c[q];
+                } else {
+                    cudaFree(A->mask);
+                    A->mask = nullptr;
+                }
+            }
         }
     }
     *out = A;
@@ -670,6 +732,11 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
                          s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
     // complex 5-point Helmholtz smoother (V-cycle fine level): blocked sweep
     const bool cblocked = !blocked && A->cblock_ok && s->precond == RG_PRECOND_NONE && block_T != 1;
+    // (large levels only: on a few CTAs the 8-points-per-thread window is
+    // latency-bound, 48 us per 4-step launch at 31^2 against 4 x 6.4 us for
+    // the one-step kernel; measured break-even between 255^2 and 511^2)
+    const bool cblocked9 = !blocked && A->var9h && s->precond == RG_PRECOND_NONE &&
+                           block_T != 1 && (block_T > 1 || A->d.side >= 384);
     std::vector<double> hscale;
     const bool jac = s->precond == RG_PRECOND_JACOBI_SCALAR;
     if (blocked && jac) {
@@ -684,8 +751,32 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     const int TC = block_T == 0 ? 4 : (block_T < 4 ? block_T : 4);
     while (left > 0) {
         const int t = blocked ? chunk_len(n_steps, T, n_steps - left)
-                              : (cblocked ? chunk_len(n_steps, TC, n_steps - left) : 1);
-        if (cblocked) {
+                              : ((cblocked || cblocked9) ? chunk_cap(n_steps, TC, n_steps - left) : 1);
+        if (cblocked9) {
+            CBlock9Args ca;
+            for (int q = 0; q < 9; ++q) ca.c9[q] = A->hc9[q];
+            ca.planes = (const double2*)A->d.stencil;
+            ca.mask = A->mask;
+            ca.side = A->d.side;
+            ca.P = A->P;
+            ca.u_in = (const double2*)u[cur];
+            ca.u_out = (double2*)u[cur ^ 1];
+            ca.v_in = (const double2*)v[cur];
+            ca.v_out = (double2*)v[cur ^ 1];
+            ca.f = (const double2*)f;
+            ca.omega = s->omega;
+            ca.alpha = s->alpha;
+            ca.atil = s->alpha_tilde;
+            ca.m = s->m;
+            ca.k0 = k;
+            cudaError_t err;
+            switch (s->variant) {
+                case RG_PLAIN: err = launch_cblock9<V_PLAIN>(ca, t, A->d.batch, st); break;
+                case RG_MOM: err = launch_cblock9<V_MOM>(ca, t, A->d.batch, st); break;
+                default: err = launch_cblock9<V_NAG>(ca, t, A->d.batch, st); break;
+            }
+            rc = err == cudaSuccess ? RG_OK : fail(RG_ECUDA, "complex 9-point sweep launch: %s", cudaGetErrorString(err));
+        } else if (cblocked) {
             CBlockArgs ca;
             for (int q = 0; q < 4; ++q) ca.off[q] = A->hoff[q];
             ca.diag = (const double2*)A->d.diag;

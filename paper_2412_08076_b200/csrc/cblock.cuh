@@ -17,6 +17,12 @@
 namespace rg {
 
 constexpr int CB_LR = 32, CB_LC = 64, CB_NW = 8;
+#ifndef CB_DIAG_REGS
+#define CB_DIAG_REGS 1
+#endif
+#ifndef CB_MINB
+#define CB_MINB 2
+#endif
 
 struct CBlockArgs {
     double2 off[4];        // off-diagonals in CSR order (-1,0),(0,-1),(0,1),(1,0)
@@ -44,7 +50,7 @@ __host__ __device__ inline int cblock_ntiles(int side, int T, int* nty) {
 }
 
 template <int VAR, int T>
-__global__ void __launch_bounds__(CB_NW * 32, 2) cblock_kernel(const __grid_constant__ CBlockArgs a) {
+__global__ void __launch_bounds__(CB_NW * 32, CB_MINB) cblock_kernel(const __grid_constant__ CBlockArgs a) {
     typedef double2 C;
     constexpr int LR = CB_LR, LC = CB_LC;
     constexpr int RPW = LR / CB_NW, CPT = LC / 32;
@@ -69,6 +75,9 @@ __global__ void __launch_bounds__(CB_NW * 32, 2) cblock_kernel(const __grid_cons
     const C c0 = a.off[0], c1 = a.off[1], c2 = a.off[2], c3 = a.off[3];
 
     C ur[RPW][CPT], vr[RPW][CPT];
+#if CB_DIAG_REGS
+    C dr[RPW][CPT];           // per-node diagonal, loaded once (constant over the T steps)
+#endif
     int gidx[RPW][CPT];       // global index of the point, -1 outside the grid
     const double at0 = NAG ? a.atil[b * a.m + (a.k0 % a.m)] : 0.0;
 #pragma unroll
@@ -86,6 +95,9 @@ __global__ void __launch_bounds__(CB_NW * 32, 2) cblock_kernel(const __grid_cons
             ur[rr][cc] = u;
             vr[rr][cc] = v;
             sf[r0 + rr][col] = in ? a.f[base + g] : szero<C>();
+#if CB_DIAG_REGS
+            dr[rr][cc] = in ? __ldg(&dg[g]) : szero<C>();
+#endif
             buf0[r0 + rr][col] = (NAG && in) ? add(u, rmul(at0, v)) : u;   // (:119)
         }
     }
@@ -115,7 +127,11 @@ __global__ void __launch_bounds__(CB_NW * 32, 2) cblock_kernel(const __grid_cons
                 const int rp = r + 1 < LR ? r + 1 : LR - 1;
                 const C wv = cur[r][cm], ev = cur[r][cp], dn = cur[rp][col];
                 const int g = gidx[rr][cc];
+#if CB_DIAG_REGS
+                const C d = dr[rr][cc];
+#else
                 const C d = g >= 0 ? __ldg(&dg[g]) : szero<C>();
+#endif
                 C s = mul(c0, up);                        // CSR order, unfused products
                 s = add(s, mul(c1, wv));
                 s = add(s, mul(d, mid));
@@ -176,6 +192,188 @@ cudaError_t launch_cblock(const CBlockArgs& a, int T, int batch, cudaStream_t st
         case 2: return launch_cblock_t<VAR, 2>(a, batch, st);
         case 3: return launch_cblock_t<VAR, 3>(a, batch, st);
         case 4: return launch_cblock_t<VAR, 4>(a, batch, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace rg
+
+namespace rg {
+
+// ---------------------------------------------------------------------------
+// 9-point complex variant for the Galerkin levels (VAR9, multigrid.py:62-68):
+// same window scheme; rows flagged in `mask` use the repeated stencil c9
+// (kernel parameters), the others read their 9 planes (L1/L2).  CSR column
+// order (-1,-1),(-1,0),(-1,1),(0,-1),(0,0),(0,1),(1,-1),(1,0),(1,1),
+// unfused complex products: bitwise the CSR matvec (apply_op<VAR9>).
+struct CBlock9Args {
+    double2 c9[9];
+    const double2* planes;        // [9][P] (one coefficient set, shared by the batch)
+    const unsigned char* mask;    // [P] 1: row == c9
+    int side, P;
+    const double2* u_in;
+    const double2* v_in;
+    double2* u_out;
+    double2* v_out;
+    const double2* f;
+    const double* omega;
+    const double* alpha;
+    const double* atil;
+    int m;
+    int k0;
+    int nty;
+};
+
+template <int VAR, int T>
+__global__ void __launch_bounds__(CB_NW * 32, 2) cblock9_kernel(const __grid_constant__ CBlock9Args a) {
+    typedef double2 C;
+    constexpr int LR = CB_LR, LC = CB_LC;
+    constexpr int RPW = LR / CB_NW, CPT = LC / 32;
+    constexpr int TX = LR - 2 * T, TY = LC - 2 * T;
+    constexpr bool NAG = VAR >= V_NAG;
+    constexpr bool HASV = VAR != V_PLAIN;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    typedef C Row[LC];
+    Row* buf0 = reinterpret_cast<Row*>(smem_raw);
+    Row* buf1 = buf0 + LR;
+    Row* sf = buf1 + LR;
+
+    const int b = blockIdx.y;
+    const int cta = blockIdx.x;
+    const int tx = cta / a.nty, ty = cta - (cta / a.nty) * a.nty;
+    const int gx0 = tx * TX - T, gy0 = ty * TY - T;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+    const int side = a.side;
+    const size_t base = (size_t)b * a.P;
+    const int r0 = wp * RPW;
+    const size_t P = a.P;
+
+    C ur[RPW][CPT], vr[RPW][CPT];
+    int gidx[RPW][CPT];       // global index, -1 outside the grid; -2 - g for band rows
+    const double at0 = NAG ? a.atil[b * a.m + (a.k0 % a.m)] : 0.0;
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+        const int gx = gx0 + r0 + rr;
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int col = lane + 32 * cc;
+            const int gy = gy0 + col;
+            const bool in = (gx >= 0) && (gx < side) && (gy >= 0) && (gy < side);
+            const int g = in ? gx * side + gy : -1;
+            gidx[rr][cc] = (in && !a.mask[g]) ? -2 - g : g;
+            const C u = in ? a.u_in[base + g] : szero<C>();
+            const C v = (HASV && in) ? a.v_in[base + g] : szero<C>();
+            ur[rr][cc] = u;
+            vr[rr][cc] = v;
+            sf[r0 + rr][col] = in ? a.f[base + g] : szero<C>();
+            buf0[r0 + rr][col] = (NAG && in) ? add(u, rmul(at0, v)) : u;
+        }
+    }
+    __syncthreads();
+
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int k = a.k0 + t;
+        const int si = b * a.m + (k % a.m);
+        const double w = a.omega[si];
+        const double al = HASV ? a.alpha[si] : 0.0;
+        const double atn = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+        Row* cur = (t & 1) ? buf1 : buf0;
+        Row* nxt = (t & 1) ? buf0 : buf1;
+        const bool last = (t == T - 1);
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int col = lane + 32 * cc;
+            const int cm = col > 0 ? col - 1 : 0;
+            const int cp = col < LC - 1 ? col + 1 : LC - 1;
+            const int rm = r0 > 0 ? r0 - 1 : 0;
+            C upw = cur[rm][cm], up = cur[rm][col], upe = cur[rm][cp];
+            C mw = cur[r0][cm], mid = cur[r0][col], me = cur[r0][cp];
+#pragma unroll
+            for (int rr = 0; rr < RPW; ++rr) {
+                const int r = r0 + rr;
+                const int rp = r + 1 < LR ? r + 1 : LR - 1;
+                const C dw = cur[rp][cm], dn = cur[rp][col], de = cur[rp][cp];
+                const int g = gidx[rr][cc];
+                C s;
+                if (g >= -1) {   // the repeated stencil (or outside the grid)
+                    s = mul(a.c9[0], upw);
+                    s = add(s, mul(a.c9[1], up));
+                    s = add(s, mul(a.c9[2], upe));
+                    s = add(s, mul(a.c9[3], mw));
+                    s = add(s, mul(a.c9[4], mid));
+                    s = add(s, mul(a.c9[5], me));
+                    s = add(s, mul(a.c9[6], dw));
+                    s = add(s, mul(a.c9[7], dn));
+                    s = add(s, mul(a.c9[8], de));
+                } else {         // band row: its own coefficient planes
+                    const C* c = a.planes + (size_t)(-2 - g);
+                    s = mul(__ldg(&c[0]), upw);
+                    s = add(s, mul(__ldg(&c[1 * P]), up));
+                    s = add(s, mul(__ldg(&c[2 * P]), upe));
+                    s = add(s, mul(__ldg(&c[3 * P]), mw));
+                    s = add(s, mul(__ldg(&c[4 * P]), mid));
+                    s = add(s, mul(__ldg(&c[5 * P]), me));
+                    s = add(s, mul(__ldg(&c[6 * P]), dw));
+                    s = add(s, mul(__ldg(&c[7 * P]), dn));
+                    s = add(s, mul(__ldg(&c[8 * P]), de));
+                }
+                const C rs = sub(sf[r][col], s);
+                C vn;
+                if (VAR == V_PLAIN) vn = rmul(w, rs);
+                else vn = add(rmul(al, vr[rr][cc]), rmul(w, rs));
+                const C un = add(NAG ? ur[rr][cc] : mid, vn);
+                if (HASV) vr[rr][cc] = vn;
+                ur[rr][cc] = un;
+                if (!last) {
+                    const C x = NAG ? add(un, rmul(atn, vn)) : un;
+                    nxt[r][col] = g != -1 ? x : szero<C>();
+                }
+                upw = mw; up = mid; upe = me;
+                mw = dw; mid = dn; me = de;
+            }
+        }
+        if (!last) __syncthreads();
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+        const int r = r0 + rr;
+#pragma unroll
+        for (int cc = 0; cc < CPT; ++cc) {
+            const int col = lane + 32 * cc;
+            int g = gidx[rr][cc];
+            if (g < -1) g = -2 - g;
+            if (g >= 0 && r >= T && r < LR - T && col >= T && col < LC - T) {
+                a.u_out[base + g] = ur[rr][cc];
+                if (HASV) a.v_out[base + g] = vr[rr][cc];
+            }
+        }
+    }
+}
+
+template <int VAR, int T>
+cudaError_t launch_cblock9_t(const CBlock9Args& a0, int batch, cudaStream_t st) {
+    auto kern = cblock9_kernel<VAR, T>;
+    const size_t smem = 3 * (size_t)CB_LR * CB_LC * sizeof(double2);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    CBlock9Args a = a0;
+    const int nt = cblock_ntiles(a.side, T, &a.nty);
+    kern<<<dim3(nt, batch), dim3(CB_NW * 32), smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int VAR>
+cudaError_t launch_cblock9(const CBlock9Args& a, int T, int batch, cudaStream_t st) {
+    switch (T) {
+        case 1: return launch_cblock9_t<VAR, 1>(a, batch, st);
+        case 2: return launch_cblock9_t<VAR, 2>(a, batch, st);
+        case 3: return launch_cblock9_t<VAR, 3>(a, batch, st);
+        case 4: return launch_cblock9_t<VAR, 4>(a, batch, st);
     }
     return cudaErrorInvalidValue;
 }

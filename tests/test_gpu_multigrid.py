@@ -159,3 +159,27 @@ def test_complex_blocked_sweep_bitwise(n, variant):
     for k in range(11):
         x = x + s.omega[k % 4] * (f[1] - A @ x)
     assert np.array_equal(ref[0][1], x)
+
+
+@pytest.mark.parametrize("n", [64, 256])
+@pytest.mark.parametrize("variant", ["plain", "mom", "nag"])
+def test_complex_galerkin_blocked_sweep_bitwise(n, variant):
+    """The blocked 9-point complex sweep of the Galerkin levels (repeated
+    stencil + band planes, cblock9_kernel) gives the one-step kernel's bits."""
+    H = O.assemble_helmholtz(2 * np.pi * n / 10, n)
+    levels, _ = O.build_hierarchy(H, n, coarsest=8)
+    Ac = levels[1]["A"]
+    B = 3
+    op = G.GpuStencilOperator.from_sparse(Ac).broadcast(B)
+    assert op.kind == 3
+    rng = np.random.default_rng(n + 1)
+    P = Ac.shape[0]
+    cplx = lambda: rng.standard_normal((B, P)) + 1j * rng.standard_normal((B, P))  # noqa: E731
+    f, u0 = cplx(), cplx()
+    v0 = cplx() if variant != "plain" else np.zeros((B, P), complex)
+    ref = _csweep(op, variant, 9, 1, f, u0, v0)
+    for T in (0, 2, 3, 4):
+        got = _csweep(op, variant, 9, T, f, u0, v0)
+        assert np.array_equal(got[0], ref[0]), (T, np.abs(got[0] - ref[0]).max())
+        if variant != "plain":
+            assert np.array_equal(got[1], ref[1])
