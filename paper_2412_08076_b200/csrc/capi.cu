@@ -21,6 +21,7 @@
 #include "cblock.cuh"
 #include "tri.cuh"
 #include "adjoint.cuh"
+#include "psweep.cuh"
 
 using namespace rg;
 
@@ -66,8 +67,12 @@ struct rg_op {
     bool var9h = false;
     double2 hc9[9];
     unsigned char* mask = nullptr;  // device [P] (owned)
+    // small-grid persistent sweep workspace (y ping-pong + grid barrier),
+    // allocated on first use outside stream capture
+    mutable void* ps_ws = nullptr;
     ~rg_op() {
         if (mask) cudaFree(mask);
+        if (ps_ws) cudaFree(ps_ws);
     }
 };
 
@@ -749,6 +754,70 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     int k = i0;
     int left = n_steps;
     const int TC = block_T == 0 ? 4 : (block_T < 4 ? block_T : 4);
+    // small grids (coarse V-cycle levels): every step in one cooperative launch
+    const size_t total = (size_t)A->d.batch * A->P;
+    // (one point per thread: a 16-CTA cluster covers 4096 unknowns; at 127^2,
+    // 4 points per thread, the cluster sweep measured slower than 16
+    // one-step launches: 129 vs 102 us)
+    bool small = !blocked && !cblocked && !cblocked9 && block_T == 0 && n_steps >= 2 &&
+                 (A->d.dtype == RG_F64 || A->d.dtype == RG_C128) && A->P <= 16 * PS_NT;
+    if (small && !A->ps_ws) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cs);
+        const size_t el = A->d.dtype == RG_C128 ? 16 : 8;
+        if (cs != cudaStreamCaptureStatusNone ||
+            cudaMalloc(&A->ps_ws, 2 * total * el + 256) != cudaSuccess) {
+            small = false;
+            A->ps_ws = nullptr;
+            cudaGetLastError();
+        }
+    }
+    if (small) {
+        const size_t el = A->d.dtype == RG_C128 ? 16 : 8;
+        char* y0 = (char*)A->ps_ws + 256;
+        char* y1 = y0 + total * el;
+        cudaError_t err;
+        if (A->d.dtype == RG_F64) {
+            PsArgs<double> pa;
+            pa.A = view<double>(A);
+            pa.u = (double*)u[0];
+            pa.v = (double*)v[0];
+            pa.f = (const double*)f;
+            pa.y0 = (double*)y0;
+            pa.y1 = (double*)y1;
+            pa.omega = s->omega;
+            pa.alpha = s->alpha;
+            pa.atil = s->alpha_tilde;
+            pa.scale = (const double*)s->scale;
+            pa.precond = s->precond;
+            pa.m = s->m;
+            pa.k0 = i0;
+            pa.n_steps = n_steps;
+            pa.B = A->d.batch;
+            err = launch_psweep(pa, A->d.kind, s->variant, st);
+        } else {
+            PsArgs<double2> pa;
+            pa.A = view<double2>(A);
+            pa.u = (double2*)u[0];
+            pa.v = (double2*)v[0];
+            pa.f = (const double2*)f;
+            pa.y0 = (double2*)y0;
+            pa.y1 = (double2*)y1;
+            pa.omega = s->omega;
+            pa.alpha = s->alpha;
+            pa.atil = s->alpha_tilde;
+            pa.scale = (const double2*)s->scale;
+            pa.precond = s->precond;
+            pa.m = s->m;
+            pa.k0 = i0;
+            pa.n_steps = n_steps;
+            pa.B = A->d.batch;
+            err = launch_psweep(pa, A->d.kind, s->variant, st);
+        }
+        if (err != cudaSuccess) return fail(RG_ECUDA, "small-grid sweep launch: %s", cudaGetErrorString(err));
+        *out_buf = 0;
+        return RG_OK;
+    }
     while (left > 0) {
         const int t = blocked ? chunk_len(n_steps, T, n_steps - left)
                               : ((cblocked || cblocked9) ? chunk_cap(n_steps, TC, n_steps - left) : 1);

@@ -1,0 +1,139 @@
+// psweep.cuh — free-running sweeps of small grids in ONE launch
+// (multigrid.py:126-138 `_smooth` on the coarse V-cycle levels, and any
+// other small rg_sweep).
+//
+// On small grids a one-step launch is latency-bound (6.4 us per step at
+// 31^2 .. 127^2 in the cfg5 V-cycle).  Here one
+// thread-block cluster per system (up to 16 CTAs) runs all the steps, with
+// a cluster barrier between steps (a grid-wide software barrier measured
+// ~4 us per step; cluster barriers are hardware): the stencil input y (u,
+// or the NAG look-ahead u + at v) ping-pongs through two L2-resident
+// buffers, u and v are updated in place (pointwise), f and the
+// coefficients stay in L2.  The arithmetic is step1_kernel's, operation for
+// operation (bitwise).  Used up to 4096 unknowns per system (one point per
+// thread); 16 smoothing steps at 63^2 take 50 us against 102 us.
+#pragma once
+#include <cooperative_groups.h>
+#include "step.cuh"
+
+namespace rg {
+
+constexpr int PS_NT = 256;
+
+template <typename S>
+struct PsArgs {
+    OpView<S> A;
+    S* u;
+    S* v;              // null for plain
+    const S* f;
+    S* y0;
+    S* y1;
+    const double* omega;
+    const double* alpha;
+    const double* atil;
+    const CT<S>* scale;
+    int precond;
+    int m, k0, n_steps, B;
+};
+
+template <typename S, int KIND, int VAR>
+__global__ void __launch_bounds__(PS_NT) psweep_kernel(const __grid_constant__ PsArgs<S> a) {
+    typedef CT<S> C;
+    constexpr bool NAG = VAR >= V_NAG;
+    constexpr bool HASV = VAR != V_PLAIN;
+    namespace cgp = cooperative_groups;
+    cgp::cluster_group cl = cgp::this_cluster();
+    const int side = a.A.side;
+    const size_t P = a.A.P;
+    const int b = blockIdx.x / cl.num_blocks();             // one cluster per system
+    const size_t nth = (size_t)cl.num_blocks() * blockDim.x;
+    const size_t gt = (size_t)cl.block_rank() * blockDim.x + threadIdx.x;
+    const size_t base = (size_t)b * P;
+    // y_0: the stencil input of step k0
+    for (size_t q = base + gt; q < base + P; q += nth) {
+        C x = to_c(a.u[q]);
+        if (NAG) x = add(x, rmul(a.atil[b * a.m + (a.k0 % a.m)], to_c(a.v[q])));
+        a.y0[q] = to_s<S>(x);
+    }
+    cl.sync();
+    for (int t = 0; t < a.n_steps; ++t) {
+        const int k = a.k0 + t;
+        const S* cur = (t & 1) ? a.y1 : a.y0;
+        S* nxt = (t & 1) ? a.y0 : a.y1;
+        for (size_t q = base + gt; q < base + P; q += nth) {
+            const size_t idx = q - base;
+            const int i = (int)(idx / side), j = (int)(idx - (size_t)i * side);
+            const S* y = cur + (size_t)b * P;
+            auto X = [&](int di, int dj) -> C {
+                const int ii = i + di, jj = j + dj;
+                if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
+                return to_c(y[idx + (ptrdiff_t)di * side + dj]);
+            };
+            const C s = apply_op<S, KIND>(a.A, b, idx, X);
+            const C r = sub(to_c(a.f[q]), s);
+            C p = r;                                           // precond.py:125-129
+            if (a.precond == P_JSCALAR) p = mul(a.scale[b], r);
+            else if (a.precond == P_JFIELD) p = mul(a.scale[q], r);
+            const int si = b * a.m + (k % a.m);
+            const double w = a.omega[si];
+            const C ui = to_c(a.u[q]);
+            C vn;
+            if (VAR == V_PLAIN) vn = rmul(w, p);
+            else vn = add(rmul(a.alpha[si], to_c(a.v[q])), rmul(w, p));
+            const S vs = to_s<S>(vn);
+            const S us = to_s<S>(add(ui, vn));
+            a.u[q] = us;
+            if (HASV) a.v[q] = vs;
+            C x = to_c(us);
+            if (NAG) x = add(x, rmul(a.atil[b * a.m + ((k + 1) % a.m)], to_c(vs)));
+            nxt[q] = to_s<S>(x);
+        }
+        cl.sync();
+    }
+}
+
+template <typename S, int KIND, int VAR>
+cudaError_t launch_psweep_t(const PsArgs<S>& a, cudaStream_t st) {
+    auto kern = psweep_kernel<S, KIND, VAR>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int cs = (int)((a.A.P + PS_NT - 1) / PS_NT);
+    cs = cs < 1 ? 1 : (cs > 16 ? 16 : cs);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.B * cs);
+    cfg.blockDim = dim3(PS_NT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <typename S, int KIND>
+cudaError_t launch_psweep_k(const PsArgs<S>& a, int variant, cudaStream_t st) {
+    switch (variant) {
+        case V_PLAIN: return launch_psweep_t<S, KIND, V_PLAIN>(a, st);
+        case V_MOM: return launch_psweep_t<S, KIND, V_MOM>(a, st);
+        default: return launch_psweep_t<S, KIND, V_NAG>(a, st);
+    }
+}
+
+template <typename S>
+cudaError_t launch_psweep(const PsArgs<S>& a, int kind, int variant, cudaStream_t st) {
+    switch (kind) {
+        case K_CONST9: return launch_psweep_k<S, K_CONST9>(a, variant, st);
+        case K_DIAG5: return launch_psweep_k<S, K_DIAG5>(a, variant, st);
+        default: return launch_psweep_k<S, K_VAR9>(a, variant, st);
+    }
+}
+
+}  // namespace rg

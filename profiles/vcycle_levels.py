@@ -34,7 +34,7 @@ def ev(fn, reps=10):
     return s.elapsed_time(e) / reps * 1e3
 
 
-out = {"vcycle_us": ev(lambda: h.apply(Fd))}
+out = {"vcycle_us": ev(lambda: h.apply(Fd)), "graphs": bool(h.use_graphs)}
 for k, lvl in enumerate(h.levels[:-1]):
     f = torch.randn(4, lvl.op.P, dtype=torch.complex128, device="cuda")
     u = torch.zeros_like(f)
