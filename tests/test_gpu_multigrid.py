@@ -108,16 +108,16 @@ def test_fgmres_plain_matches_oracle():
     assert _rel(u, uo) <= 1e-7
 
 
-def _csweep(op, variant, n_steps, block_T, f, u0, v0, seed=0):
-    """rg_sweep on a complex DIAG5 operator, returns (u, v) on the host."""
+def _csweep(op, variant, n_steps, block_T, f, u0, v0, seed=0, P=None, lam=None):
+    """rg_sweep on a stencil operator, returns (u, v) on the host."""
     import ctypes as C
     m = 4
     rng = np.random.default_rng(seed)
-    lam = 8.0 * op.side ** 2
+    lam = 8.0 * op.side ** 2 if lam is None else lam
     w = rng.uniform(0.2, 0.9, m) / lam
     kw = {} if variant == "plain" else {"alpha": np.full(m, 0.35)}
     from paper_2412_08076_b200.richardson import DeviceSchedule
-    sch = DeviceSchedule(op, G.WeightSchedule(omega=w, variant=variant, **kw))
+    sch = DeviceSchedule(op, G.WeightSchedule(omega=w, variant=variant, **kw), P)
     dev = op.device
     t = lambda a: torch.as_tensor(a).to(dev).clone()
     u = [t(u0), torch.empty_like(t(u0))]
@@ -181,5 +181,35 @@ def test_complex_galerkin_blocked_sweep_bitwise(n, variant):
     for T in (0, 2, 3, 4):
         got = _csweep(op, variant, 9, T, f, u0, v0)
         assert np.array_equal(got[0], ref[0]), (T, np.abs(got[0] - ref[0]).max())
+        if variant != "plain":
+            assert np.array_equal(got[1], ref[1])
+
+
+
+@pytest.mark.parametrize("variant", ["plain", "mom", "nag"])
+@pytest.mark.parametrize("pre", [None, "field"])
+def test_small_grid_resident_sweep_bitwise(variant, pre):
+    """Small grids run every step in one cluster-resident launch
+    (psweep_kernel): same bits as the one-step kernel, real VAR9 and DIAG5
+    operators, with and without a per-node Jacobi scale."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(17)
+    A = O.assemble_anisotropic(0.1, 0.7, 24)
+    A9 = (sp.diags(rng.uniform(0.5, 1.5, A.shape[0])) @ A).tocsr()        # VAR9
+    H = O.assemble_helmholtz(20.0, 40)
+    A5 = sp.csr_matrix((H.data.real.copy(), H.indices, H.indptr), shape=H.shape)   # real DIAG5
+    for M in (A9, A5):
+        B = 2
+        op = G.GpuStencilOperator.from_sparse(M).broadcast(B)
+        P = None
+        if pre == "field":
+            P = G.JacobiScale((2.0 / 3.0) / M.diagonal())
+        n = M.shape[0]
+        f, u0 = rng.standard_normal((B, n)), rng.standard_normal((B, n))
+        v0 = rng.standard_normal((B, n)) if variant != "plain" else np.zeros((B, n))
+        lam = np.abs(M.diagonal()).max() * 2.5
+        ref = _csweep(op, variant, 7, 1, f, u0, v0, P=P, lam=lam)
+        got = _csweep(op, variant, 7, 0, f, u0, v0, P=P, lam=lam)
+        assert np.array_equal(got[0], ref[0])
         if variant != "plain":
             assert np.array_equal(got[1], ref[1])
