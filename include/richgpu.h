@@ -195,7 +195,10 @@ int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void*
  * ~1e-15; the reference's own bar is 1e-13).  relax in (0, 2); a zero
  * diagonal is RG_EINVAL (ZeroDiagonalError).  work: [batch][side*side]
  * scratch for SSOR (may be NULL for SOR).  r and z must not alias. */
-enum rg_tri { RG_TRI_SOR = 1, RG_TRI_SSOR = 2 };
+enum rg_tri { RG_TRI_SOR = 1, RG_TRI_SSOR = 2,
+              /* the transposed maps B^{-T} (Preconditioner.apply_transpose,
+               * precond.py:94,112-113), used by the training adjoint */
+              RG_TRI_SOR_T = 3, RG_TRI_SSOR_T = 4 };
 int rg_tri_apply(const rg_op* A, int kind, double relax, const void* r, void* z,
                  void* work, void* stream);
 /* The Richardson update from an externally preconditioned residual z
@@ -223,6 +226,16 @@ int rg_unroll_adjoint_step(const rg_op* A, const rg_op* At, const rg_sched* s,
                            int i, const void* f, const void* u_k, const void* v_k,
                            void* ubar, void* vbar, void* rbar, double* dots,
                            void* stream);
+
+/* The same reverse step with a GS / SOR / SSOR preconditioner, in two
+ * phases around the host's rg_tri_apply(RG_TRI_*_T, rbar_pre -> rbar):
+ * phase 1 reads p_k (the forward's B^{-1} r_k history) and writes
+ * rbar_pre = w_i vbar_total and dots[0..1][batch]; phase 2 reads rbar
+ * (= B^{-T} rbar_pre), updates ubar / vbar and writes dots[2][batch]. */
+int rg_unroll_adjoint_step_ext(const rg_op* A, const rg_op* At, const rg_sched* s,
+                               int i, const void* v_k, const void* p_k, void* ubar,
+                               void* vbar, void* rbar_pre, void* rbar, double* dots,
+                               int phase, void* stream);
 
 /* ---- solve_stationary engine (richardson.py:77-141) ----------------------
  * A solver owns device workspace (per-system status, trace, reduction

@@ -18,7 +18,7 @@ RG_CONST9, RG_DIAG5, RG_VAR9 = 1, 2, 3
 RG_PLAIN, RG_MOM, RG_NAG, RG_NAGEX = 0, 1, 2, 3
 RG_PRECOND_NONE, RG_PRECOND_JACOBI_SCALAR, RG_PRECOND_JACOBI_FIELD = 0, 1, 2
 RG_CHECK_OUTER, RG_CHECK_INNER = 0, 1
-RG_TRI_SOR, RG_TRI_SSOR = 1, 2
+RG_TRI_SOR, RG_TRI_SSOR, RG_TRI_SOR_T, RG_TRI_SSOR_T = 1, 2, 3, 4
 RG_ACTIVE, RG_CONVERGED, RG_DIVERGED, RG_MAXED = 0, 1, 2, 3
 RG_OK, RG_EINVAL, RG_ESIZE, RG_ENULL, RG_EUNSUPPORTED, RG_ECUDA, RG_ESTATE = 0, -1, -2, -3, -4, -5, -6
 
@@ -57,6 +57,8 @@ _SIGS = [
     ("rg_unroll_adjoint_init", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("rg_unroll_adjoint_step", _I, [_P, _P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P, _P, _P,
                                     _P]),
+    ("rg_unroll_adjoint_step_ext", _I, [_P, _P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P, _P,
+                                        _P, _I, _P]),
     ("rg_precond_update", _I, [_P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P]),
     ("rg_sweep", _I, [_P, C.POINTER(rg_sched), _I, _I, _I, _P, _P, _P, _P, _P, C.POINTER(_I), _P]),
     ("rg_dst_create", _I, [C.POINTER(_P), _I, _I]),

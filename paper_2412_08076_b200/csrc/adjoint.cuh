@@ -13,7 +13,9 @@
 //     dL/dat_i += <ybar, v_k>    (nag/nagex)
 // Two kernels per step (the second needs rbar at the neighbours); the three
 // inner products are per-CTA partials summed in a fixed order (deterministic,
-// not BLAS-bitwise).  Real float64 operators; P = identity or Jacobi.
+// not BLAS-bitwise).  Real float64 operators; P = identity or Jacobi inline,
+// GS / SOR / SSOR through the two-phase entry (adj_a_ext_kernel, then the
+// host's transposed triangular solve, then adj_b_kernel).
 #pragma once
 #include "step.cuh"
 
@@ -32,11 +34,36 @@ struct AdjArgs {
     const double* alpha;    // may be null (plain)
     const double* atil;     // may be null unless nag/nagex
     const double* scale;    // Jacobi: [B] (JSCALAR) or [B][P] (JFIELD)
+    const double* pk;       // external preconditioner: p_k history [B][P] (EXT pass)
+    double* rbar_pre;       // external preconditioner: w vt, before P^T (EXT pass)
     int precond;
     int m, i;
     int nag;
     double* part;           // [3][B][ncta]
 };
+
+// pass 1 with an external (GS/SOR/SSOR) preconditioner: p_k from the forward
+// history, rbar_pre = w vt (the host applies P^T with rg_tri_apply)
+__global__ void __launch_bounds__(STEP_NT) adj_a_ext_kernel(AdjArgs a) {
+    const int b = blockIdx.z;
+    const int side = a.A.side;
+    const int cta = blockIdx.x + gridDim.x * blockIdx.y;
+    const int ncta = gridDim.x * gridDim.y;
+    const int j = blockIdx.x * STEP_BX + threadIdx.x;
+    const int i = blockIdx.y * STEP_BY + threadIdx.y;
+    const size_t base = (size_t)b * a.A.P;
+    const int si = b * a.m + a.i;
+    double d1 = 0.0, d2 = 0.0;
+    if (i < side && j < side) {
+        const size_t q = base + (size_t)i * side + j;
+        const double vt = a.vbar[q] + a.ubar[q];
+        d1 = vt * a.v[q];
+        d2 = vt * a.pk[q];
+        a.rbar_pre[q] = a.omega[si] * vt;
+    }
+    write_partial<STEP_NT>(a.part + ((size_t)0 * gridDim.z + b) * ncta, cta, d1);
+    write_partial<STEP_NT>(a.part + ((size_t)1 * gridDim.z + b) * ncta, cta, d2);
+}
 
 // pass 1: p_k at the point (stencil of y_k), vt, rbar; partials <vt,v_k>, <vt,p_k>
 template <int KIND>

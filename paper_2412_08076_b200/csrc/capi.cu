@@ -583,9 +583,10 @@ int rg_tri_apply(const rg_op* A, int kind, double relax, const void* r, void* z,
     if (rc) return rc;
     if (A->d.kind != RG_CONST9 || A->d.dtype == RG_C128)
         return fail(RG_EUNSUPPORTED, "GS/SOR/SSOR need a CONST9 real operator");
-    if (kind != RG_TRI_SOR && kind != RG_TRI_SSOR) return fail(RG_EINVAL, "bad triangular kind %d", kind);
+    if (kind < RG_TRI_SOR || kind > RG_TRI_SSOR_T) return fail(RG_EINVAL, "bad triangular kind %d", kind);
+    const bool needs_work = kind == RG_TRI_SSOR || kind == RG_TRI_SSOR_T;
     if (!(relax > 0.0 && relax < 2.0)) return fail(RG_EINVAL, "relaxation must be in (0, 2), got %g", relax);
-    if (!r || !z || (kind == RG_TRI_SSOR && !work)) return fail(RG_ENULL, "null vector");
+    if (!r || !z || (needs_work && !work)) return fail(RG_ENULL, "null vector");
     if (r == z || work == r || work == z) return fail(RG_EINVAL, "r, z and work must not alias");
     for (int b = 0; b < (A->d.shared ? 1 : A->d.batch); ++b)
         if (A->hcoef[(size_t)b * 9 + 4] == 0.0) return fail(RG_EINVAL, "zero diagonal entry in system %d", b);
@@ -714,6 +715,54 @@ int rg_unroll_adjoint_step(const rg_op* A, const rg_op* At, const rg_sched* s, i
         adj_b_kernel<KIND><<<g, blk, 0, st>>>(a);
         sum_partials_kernel<256><<<3 * B, 256, 0, st>>>(a.part, ncta, dots);
     });
+    if (e != cudaSuccess) rc = fail(RG_ECUDA, "adjoint step launch: %s", cudaGetErrorString(e));
+    CUDA_TRY(cudaFreeAsync(a.part, st));
+    return rc;
+}
+
+int rg_unroll_adjoint_step_ext(const rg_op* A, const rg_op* At, const rg_sched* s, int i,
+                               const void* v_k, const void* p_k, void* ubar, void* vbar,
+                               void* rbar_pre, void* rbar, double* dots, int phase, void* stream) {
+    int rc = check_adj_ops(A, At);
+    if (rc) return rc;
+    if ((rc = check_sched(A, s))) return rc;
+    if (i < 0 || i >= s->m) return fail(RG_EINVAL, "inner index %d outside [0, %d)", i, s->m);
+    if (phase != 1 && phase != 2) return fail(RG_EINVAL, "phase must be 1 or 2");
+    if (!v_k || !ubar || !vbar || !dots || (phase == 1 && (!p_k || !rbar_pre)) || (phase == 2 && !rbar))
+        return fail(RG_ENULL, "null argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const dim3 g = step_grid(A), blk(STEP_BX, STEP_BY);
+    const int ncta = g.x * g.y, B = A->d.batch;
+    AdjArgs a;
+    memset(&a, 0, sizeof a);
+    a.A = view<double>(A);
+    a.At = view<double>(At);
+    a.v = (const double*)v_k;
+    a.pk = (const double*)p_k;
+    a.ubar = (double*)ubar;
+    a.vbar = (double*)vbar;
+    a.rbar = (double*)rbar;
+    a.rbar_pre = (double*)rbar_pre;
+    a.omega = s->omega;
+    a.alpha = s->variant == RG_PLAIN ? nullptr : s->alpha;
+    a.atil = s->alpha_tilde;
+    a.m = s->m;
+    a.i = i;
+    a.nag = s->variant >= RG_NAG;
+    ensure_pool();
+    CUDA_TRY(cudaMallocAsync((void**)&a.part, sizeof(double) * 3 * B * ncta, st));
+    cudaError_t e;
+    if (phase == 1) {
+        adj_a_ext_kernel<<<g, blk, 0, st>>>(a);
+        sum_partials_kernel<256><<<2 * B, 256, 0, st>>>(a.part, ncta, dots);
+        e = cudaGetLastError();
+    } else {
+        e = by_kind(A->d.kind, [&](auto kk) {
+            constexpr int KIND = decltype(kk)::value;
+            adj_b_kernel<KIND><<<g, blk, 0, st>>>(a);
+            sum_partials_kernel<256><<<B, 256, 0, st>>>(a.part + (size_t)2 * B * ncta, ncta, dots + 2 * B);
+        });
+    }
     if (e != cudaSuccess) rc = fail(RG_ECUDA, "adjoint step launch: %s", cudaGetErrorString(e));
     CUDA_TRY(cudaFreeAsync(a.part, st));
     return rc;

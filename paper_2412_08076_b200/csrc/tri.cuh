@@ -28,7 +28,12 @@
 
 namespace rg {
 
-enum { TRI_SOR = 1, TRI_SSOR = 2 };
+enum { TRI_SOR = 1, TRI_SSOR = 2, TRI_SOR_T = 3, TRI_SSOR_T = 4 };
+// Transposed maps (P.apply_transpose, precond.py:93-94,112-113; the training
+// adjoint): (D + wL)^T has row i coupled to rows below at the mirrored
+// lower coefficients, so relax (D + wL)^{-T} r is the reverse-order sweep
+// with the lower coefficients, and (D + wU)^{-T} the forward sweep with the
+// upper ones.
 constexpr int TRI_PF = 8;
 
 template <typename S>
@@ -203,6 +208,18 @@ __global__ void __launch_bounds__(1024, 1) tri_kernel(const TriArgs<S> a) {
         // relax * solve(r)  (precond.py:93)
         tri_sweep<false, false, true, S, S>(a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
                                             lo3, d, edge, xfer, stage);
+    } else if (MODE == TRI_SOR_T) {
+        // relax * solve_t(r)  (precond.py:94)
+        tri_sweep<true, false, true, S, S>(a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
+                                           lo3, d, edge, xfer, stage);
+    } else if (MODE == TRI_SSOR_T) {
+        // c * dlt(diag * dut(r))  (precond.py:112-113)
+        const double cc = w * (2.0 - w);
+        tri_sweep<false, false, false, S, S>(a.r + base, a.work + base, a.side, a.P, 1.0, up0, up1,
+                                             up2, up3, d, edge, xfer, stage);
+        __syncthreads();
+        tri_sweep<true, true, true, S, S>(a.work + base, a.z + base, a.side, a.P, cc, lo0, lo1, lo2,
+                                          lo3, d, edge, xfer, stage);
     } else {
         // c * du(diag * dl(r))  (precond.py:109-110)
         const double cc = w * (2.0 - w);
@@ -230,8 +247,12 @@ cudaError_t launch_tri_m(const TriArgs<S>& a, int batch, cudaStream_t st) {
 
 template <typename S>
 cudaError_t launch_tri(const TriArgs<S>& a, int mode, int batch, cudaStream_t st) {
-    return mode == TRI_SOR ? launch_tri_m<S, TRI_SOR>(a, batch, st)
-                           : launch_tri_m<S, TRI_SSOR>(a, batch, st);
+    switch (mode) {
+        case TRI_SOR: return launch_tri_m<S, TRI_SOR>(a, batch, st);
+        case TRI_SOR_T: return launch_tri_m<S, TRI_SOR_T>(a, batch, st);
+        case TRI_SSOR_T: return launch_tri_m<S, TRI_SSOR_T>(a, batch, st);
+        default: return launch_tri_m<S, TRI_SSOR>(a, batch, st);
+    }
 }
 
 // Richardson update from an externally preconditioned residual z

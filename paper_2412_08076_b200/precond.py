@@ -55,22 +55,33 @@ class TriangularPreconditioner:
         self._relax = float(relax)
         self.mode = _TRI_KINDS[kind]
 
-    def apply_device(self, r, z=None, work=None):
-        """z = B^{-1} r for device tensors [B, P] (allocates z / work if None)."""
+    def apply_device(self, r, z=None, work=None, transpose=False):
+        """z = B^{-1} r (or B^{-T} r) for device tensors [B, P]."""
         op = self.op
         z = torch.empty_like(r) if z is None else z
-        if self.mode == L.RG_TRI_SSOR and work is None:
+        mode = self.mode
+        if transpose:
+            mode = L.RG_TRI_SSOR_T if mode == L.RG_TRI_SSOR else L.RG_TRI_SOR_T
+        if mode in (L.RG_TRI_SSOR, L.RG_TRI_SSOR_T) and work is None:
             work = torch.empty_like(r)
-        L.check(op._lib.rg_tri_apply(op.handle, self.mode, self._relax, L.ptr(r), L.ptr(z),
+        L.check(op._lib.rg_tri_apply(op.handle, mode, self._relax, L.ptr(r), L.ptr(z),
                                      L.ptr(work), L.stream_ptr()))
         return z
 
-    def apply(self, r):
+    def _host_apply(self, r, transpose):
         host = not (isinstance(r, torch.Tensor) and r.is_cuda)
         rd = self.op.to_device(r)
-        z = self.apply_device(rd.reshape(self.op.batch, self.op.P))
+        z = self.apply_device(rd.reshape(self.op.batch, self.op.P), transpose=transpose)
         z = z.reshape(rd.shape)
         return z.cpu().numpy().reshape(np.shape(r)) if host else z
+
+    def apply(self, r):
+        """B^{-1} r (precond.py:56-57)."""
+        return self._host_apply(r, False)
+
+    def apply_transpose(self, r):
+        """B^{-T} r (precond.py:59-61, used by reverse-mode differentiation)."""
+        return self._host_apply(r, True)
 
     __call__ = apply
 

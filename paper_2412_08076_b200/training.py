@@ -23,7 +23,9 @@ Var), so its alpha gradient is d_alpha + d_alpha_t.
 Iterates are bitwise those of the reference's forward (same kernels as
 solve_stationary); the loss and gradients agree to ~1e-12 relative (the
 reductions are fixed-order tree sums, not NumPy's).  float64, CONST9/VAR9
-operators, P = None or weighted Jacobi.
+operators, P = None, weighted Jacobi, or GS / SOR / SSOR (TrainConfig.precond
+"gs" / "ssor", training.py:47-58): the forward keeps p_k = B^{-1} r_k and the
+reverse pass applies B^{-T} with the transposed wavefront solves.
 """
 from __future__ import annotations
 
@@ -71,11 +73,16 @@ class UnrollEngine:
             raise UnsupportedOperator("the training unroll runs on float64 CONST9/VAR9 operators")
         if K < 0:
             raise ValueError("unroll must be >= 0")
-        kind = getattr(P, "kind", None)
-        if P is not None and kind not in ("weighted-jacobi", "identity") and \
-                not hasattr(P, "scale"):
+        from .precond import TriangularPreconditioner, tri_spec
+        self.tri = None
+        spec = tri_spec(P)
+        if spec is not None:          # GS / SOR / SSOR (TrainConfig.precond "gs" / "ssor")
+            self.tri = TriangularPreconditioner(op, *spec)
+            P = None
+        elif P is not None and getattr(P, "kind", None) not in ("weighted-jacobi", "identity") \
+                and not hasattr(P, "scale"):
             raise UnsupportedOperator(
-                f"preconditioner {kind!r}: the GPU unroll supports None and weighted Jacobi")
+                f"preconditioner {getattr(P, 'kind', None)!r} has no GPU unroll path")
         self.op, self.K, self.variant, self.P = op, int(K), variant, P
         self.opT = op.transpose()
         B, n = op.batch, op.P
@@ -89,6 +96,12 @@ class UnrollEngine:
         self.loss = torch.empty(B, dtype=torch.float64, device=dev)
         self.dots = torch.empty((max(self.K, 1), 3, B), dtype=torch.float64, device=dev)
         self.ds = None
+        if self.tri is not None:      # p_k = B^{-1} r_k history and scratch
+            self.Pk = torch.empty((max(self.K, 1), B, n), dtype=torch.float64, device=dev)
+            self.r = torch.empty_like(self.f)
+            self.y = torch.empty_like(self.f)
+            self.work = torch.empty_like(self.f)
+            self.rpre = torch.empty_like(self.f)
 
     def forward(self, F, omega, alpha=None, alpha_t=None):
         """Loss per system (device tensor [B]) of the K-step unroll from 0."""
@@ -103,10 +116,25 @@ class UnrollEngine:
         lib, s = op._lib, L.stream_ptr()
         sched = C.byref(self.ds.struct)
         m = self.ds.m
+        nag = self.variant in ("nag", "nagex")
         for k in range(self.K):
-            L.check(lib.rg_inner_update(op.handle, sched, k % m, L.ptr(self.U[k]),
-                                        L.ptr(self.V[k]), L.ptr(self.U[k + 1]),
-                                        L.ptr(self.V[k + 1]), L.ptr(self.f), None, 0, s))
+            if self.tri is None:
+                L.check(lib.rg_inner_update(op.handle, sched, k % m, L.ptr(self.U[k]),
+                                            L.ptr(self.V[k]), L.ptr(self.U[k + 1]),
+                                            L.ptr(self.V[k + 1]), L.ptr(self.f), None, 0, s))
+                continue
+            # r_k at u_k (or the look-ahead), p_k = B^{-1} r_k kept, then the update
+            x = self.U[k]
+            if nag:
+                L.check(lib.rg_precond_update(op.handle, sched, k % m, None, L.ptr(self.U[k]),
+                                              L.ptr(self.V[k]), L.ptr(self.y), s))
+                x = self.y
+            L.check(lib.rg_residual(op.handle, L.ptr(x), L.ptr(self.f), L.ptr(self.r), None, s))
+            self.tri.apply_device(self.r, self.Pk[k], self.work)
+            self.U[k + 1].copy_(self.U[k])
+            self.V[k + 1].copy_(self.V[k])
+            L.check(lib.rg_precond_update(op.handle, sched, k % m, L.ptr(self.Pk[k]),
+                                          L.ptr(self.U[k + 1]), L.ptr(self.V[k + 1]), None, s))
         L.check(lib.rg_unroll_adjoint_init(op.handle, self.opT.handle, L.ptr(self.U[self.K]),
                                            L.ptr(self.f), L.ptr(self.rbar), L.ptr(self.ubar),
                                            L.ptr(self.vbar), L.ptr(self.loss), s))
@@ -118,11 +146,29 @@ class UnrollEngine:
         op, m = self.op, self.ds.m
         lib, s = op._lib, L.stream_ptr()
         sched = C.byref(self.ds.struct)
+        tkind = None
+        if self.tri is not None:
+            tkind = L.RG_TRI_SSOR_T if self.tri.mode == L.RG_TRI_SSOR else L.RG_TRI_SOR_T
         for k in range(self.K - 1, -1, -1):
-            L.check(lib.rg_unroll_adjoint_step(op.handle, self.opT.handle, sched, k % m,
-                                               L.ptr(self.f), L.ptr(self.U[k]), L.ptr(self.V[k]),
-                                               L.ptr(self.ubar), L.ptr(self.vbar),
-                                               L.ptr(self.rbar), L.ptr(self.dots[k]), s))
+            if self.tri is None:
+                L.check(lib.rg_unroll_adjoint_step(op.handle, self.opT.handle, sched, k % m,
+                                                   L.ptr(self.f), L.ptr(self.U[k]),
+                                                   L.ptr(self.V[k]), L.ptr(self.ubar),
+                                                   L.ptr(self.vbar), L.ptr(self.rbar),
+                                                   L.ptr(self.dots[k]), s))
+                continue
+            # p_k from the history; rbar = B^{-T} (w vt) (precond.py:94,112-113)
+            L.check(lib.rg_unroll_adjoint_step_ext(op.handle, self.opT.handle, sched, k % m,
+                                                   L.ptr(self.V[k]), L.ptr(self.Pk[k]),
+                                                   L.ptr(self.ubar), L.ptr(self.vbar),
+                                                   L.ptr(self.rpre), None, L.ptr(self.dots[k]),
+                                                   1, s))
+            L.check(lib.rg_tri_apply(op.handle, tkind, self.tri._relax, L.ptr(self.rpre),
+                                     L.ptr(self.rbar), L.ptr(self.work), s))
+            L.check(lib.rg_unroll_adjoint_step_ext(op.handle, self.opT.handle, sched, k % m,
+                                                   L.ptr(self.V[k]), None, L.ptr(self.ubar),
+                                                   L.ptr(self.vbar), None, L.ptr(self.rbar),
+                                                   L.ptr(self.dots[k]), 2, s))
         D = self.dots[:self.K].cpu().numpy()         # [K, 3, B]
         B = op.batch
         da, dw, dat = (np.zeros((B, m)) for _ in range(3))
@@ -139,8 +185,9 @@ class UnrollEngine:
 
 
 def _engine_for(A, f, K, variant, P):
+    from .precond import tri_spec
     op = A if isinstance(A, GpuStencilOperator) else as_operator(A)
-    if P is not None:
+    if P is not None and tri_spec(P) is None:
         precond_scale(P, op.P)   # validates the kind (Jacobi / identity)
     return UnrollEngine(op, K, variant, P)
 

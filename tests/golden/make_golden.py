@@ -342,17 +342,23 @@ def unroll():
     rng = np.random.default_rng(31)
     out = {}
     cases = [("plain", None), ("mom", None), ("nag", None), ("nagex", None),
-             ("plain", "jacobi"), ("nag", "jacobi"), ("mom", "jacobi")]
+             ("plain", "jacobi"), ("nag", "jacobi"), ("mom", "jacobi"),
+             ("nagex", "ssor"), ("plain", "gs"), ("mom", "ssor")]
     for k, (variant, pre) in enumerate(cases):
         n = int(rng.choice([12, 17]))
         eps, th = float(10 ** rng.uniform(-2, 0)), float(rng.uniform(0, np.pi))
         A = R.assemble_anisotropic(R.AnisotropicProblem(eps, th, n))
         f = rng.standard_normal(A.ncols)
         m, K = 3, 11
-        P = R.Preconditioner.weighted_jacobi(A) if pre == "jacobi" else None
+        P = {"jacobi": lambda: R.Preconditioner.weighted_jacobi(A),
+             "ssor": lambda: R.Preconditioner.ssor(A, relax=1.0),       # training.py:52-53
+             "gs": lambda: R.Preconditioner.gauss_seidel(A)}.get(pre, lambda: None)()
         lam = np.linalg.eigvalsh(A.to_dense()).max()
         scale = (2.0 / 3.0) / A.diagonal()[0] if pre == "jacobi" else 1.0
-        w = rng.uniform(0.3, 0.9, m) / (lam * scale)
+        if pre in ("ssor", "gs"):
+            w = rng.uniform(0.3, 0.9, m)       # B^{-1} A has its spectrum in (0, 1]
+        else:
+            w = rng.uniform(0.3, 0.9, m) / (lam * scale)
         a = rng.uniform(0.1, 0.5, m)
         at = rng.uniform(0.1, 0.5, m) if variant == "nagex" else a.copy()
         tape = Tape()

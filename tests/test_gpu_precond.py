@@ -168,3 +168,32 @@ def test_device_tensors_and_errors():
     H = O.assemble_helmholtz(10.0, 16)
     with pytest.raises(G.UnsupportedOperator):
         G.Preconditioner.ssor(H)
+
+
+def test_apply_transpose_matches_dense_transpose():
+    """B^{-T} on a non-symmetric constant stencil (anisotropic + a constant
+    convection term) equals the transpose of the assembled B^{-1}
+    (test_precond.py:66-72: 1e-12)."""
+    import scipy.sparse as sp
+    n = 10
+    A = O.assemble_anisotropic(0.2, 0.6, n).tolil()
+    s = n - 1
+    for i in range(s):
+        for j in range(s):
+            k = i * s + j
+            if j + 1 < s:
+                A[k, k + 1] += 0.3
+            if j > 0:
+                A[k, k - 1] -= 0.3
+    A = sp.csr_matrix(A)
+    op = G.GpuStencilOperator.from_sparse(A)
+    assert op.kind == 1
+    for P in (G.Preconditioner.sor(op, 1.2), G.Preconditioner.ssor(op, 0.9),
+              G.Preconditioner.gauss_seidel(op)):
+        E = np.eye(A.shape[0])
+        Bm = np.column_stack([P.apply(e) for e in E])
+        Bt = np.column_stack([P.apply_transpose(e) for e in E])
+        assert np.abs(Bt - Bm.T).max() <= 1e-12
+        kind = "gauss-seidel" if P.kind == "gauss-seidel" else P.kind
+        ref = np.column_stack([O.tri_precond(A, kind, P._relax)(e) for e in E])
+        assert np.abs(Bm - ref).max() <= 1e-13

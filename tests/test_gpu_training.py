@@ -26,7 +26,10 @@ def test_unroll_matches_reference_tape(golden):
     for k in range(int(d["count"])):
         g = lambda key: d[f"u{k}_{key}"]  # noqa: E731
         A = O.assemble_anisotropic(float(g("eps")), float(g("theta")), int(g("n")))
-        P = G.JacobiScale.weighted_jacobi(A) if str(g("pre")) == "jacobi" else None
+        pre = str(g("pre"))
+        P = {"jacobi": lambda: G.JacobiScale.weighted_jacobi(A),
+             "ssor": lambda: G.Preconditioner.ssor(A, 1.0),
+             "gs": lambda: G.Preconditioner.gauss_seidel(A)}.get(pre, lambda: None)()
         variant = str(g("variant"))
         al = g("alpha") if variant != "plain" else None
         loss, dw, da, dat = T.unrolled_residual_grad(A, g("f"), g("omega"), al, g("alpha_t"),
