@@ -317,7 +317,11 @@ inline void cluster_shape(int side, int* nc, int* rows, int* ppt) {
     const long long P = (long long)side * side;
     int c = 1;
     if (P > 4096) { *nc = 0; return; }   // larger grids: the tiled blocked sweep is faster
-    while (c < CL_MAXC && P > (long long)c * 512) c *= 2;      // ~2+ points per thread
+    // ~1+ point per thread: per-step time is the serial work per thread
+    // (cfg1 63^2: 16 CTAs 2.65 ms, 8 CTAs 3.03 ms, 4 CTAs 3.42 ms)
+    long long per = 256;
+    if (const char* ev = getenv("RG_CL_POINTS")) per = atoll(ev);   // tuning override
+    while (c < CL_MAXC && P > (long long)c * per) c *= 2;
     while (c > 1 && (side + c - 1) / c < 2) c /= 2;             // >= 2 rows per CTA
     const int R = (side + c - 1) / c;
     if ((long long)R * side > 16LL * CL_NT || (c - 1) * R >= side) { *nc = 0; return; }
