@@ -14,7 +14,8 @@
 //   -> every thread sums the partials in the same order and takes the same
 //   convergence / divergence / max_outer decision.
 // plain/mom pipeline the decision one step behind (one cluster barrier per
-// step, register backup of the previous iterate); nag uses two.
+// step, ping-ponged u) and push their boundary rows into the neighbours'
+// halo rows before the barrier; nag uses two barriers.
 //
 // Nothing touches HBM between the initial load and the final store, and
 // there is no launch per step: the solve is bound by FP64 issue and the
@@ -218,18 +219,26 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
             const double al = HASV ? a.alpha[b * m + i] : 0.0;
             const C* Uo = Ub[k & 1];
             C* Un = Ub[(k + 1) & 1];
+            C* up_nb = crank > 0 ? cl.map_shared_rank(Un, crank - 1) : nullptr;
+            C* dn_nb = crank < nc - 1 ? cl.map_shared_rank(Un, crank + 1) : nullptr;
 #pragma unroll
             for (int j = 0; j < PPT; ++j) {                     // (:120-121)
-                if (tid + j * CL_NT < npts) {
+                const int pp = tid + j * CL_NT;
+                if (pp < npts) {
                     const C p = JAC ? mul(sc, rr[j]) : rr[j];
                     C vn = (VAR == V_PLAIN) ? rmul(w, p) : add(rmul(al, vr[j]), rmul(w, p));
-                    Un[pix[j]] = stored<S>(add(Uo[pix[j]], vn));
+                    const C un = stored<S>(add(Uo[pix[j]], vn));
+                    Un[pix[j]] = un;
                     vr[j] = stored<S>(vn);
+                    // push boundary rows straight into the neighbours' halo
+                    // rows of Un (DSMEM stores, visible after the barrier):
+                    // no halo read after it.  Safe: the neighbours last read
+                    // those halo rows one barrier earlier (ping-pong).
+                    if (pp < s && up_nb) up_nb[(R + 1) * W + pix[j] - W] = un;
+                    if (pp >= npts - s && dn_nb) dn_nb[pix[j] - nrows * W] = un;
                 }
             }
             cl.sync();
-            halo(Un);
-            __syncthreads();
             {   // partial of r_{k+1} -> parts2[(k+1)&1] in every CTA
                 double v = residual_of(Un);
                 const int lane = tid & 31, wq = tid >> 5;
@@ -237,11 +246,11 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
                 for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
                 if (lane == 0) red[wq] = v;
                 __syncthreads();
-                if (tid == 0) {
+                if (tid < nc) {           // thread r publishes to CTA r (parallel DSMEM stores)
                     double t = 0.0;
 #pragma unroll
                     for (int q = 0; q < CL_NT / 32; ++q) t += red[q];
-                    for (int r = 0; r < nc; ++r) *cl.map_shared_rank(&parts2[(k + 1) & 1][crank], r) = t;
+                    *cl.map_shared_rank(&parts2[(k + 1) & 1][crank], tid) = t;
                 }
             }
             if (have_prev) {              // decide for r_k (published last iteration)
