@@ -118,7 +118,10 @@ def run_cfg2():
         t = cuda_time(go)
         res = S.results(like_numpy=True)
         out[name] = {"time_s": t, "updates_per_s": upd / t,
-                     "hbm_frac_at_40B": (upd / t) * (40 if dt == np.float64 else 20) / (HBM * 1e9)}
+                     "hbm_frac_at_40B": (upd / t) * (40 if dt == np.float64 else 20) / (HBM * 1e9),
+                     "note": "u, v, f of 64 x 255^2 = %d MB: L2-resident (126 MB L2); the fraction "
+                             "counts algorithmic bytes against the HBM peak" %
+                             (3 * 64 * 255 * 255 * (8 if dt == np.float64 else 4) // 2**20)}
         out[name]["_u"] = [res[b][0] for b in range(len(probs))]
     # parity over all 64 systems: oracle runs in parallel (f64 bitwise, f32 rel)
     procs = min(16, len(os.sched_getaffinity(0)))
