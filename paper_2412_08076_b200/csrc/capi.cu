@@ -357,6 +357,16 @@ static int chunk_len(int n, int T, int i) {
     return 1;
 }
 
+// smallest side that takes the blocked 9-point complex sweep automatically
+static int cb9_min_side() {
+    static int v = -1;
+    if (v < 0) {
+        const char* ev = getenv("RG_CB9_MINSIDE");   // tuning override
+        v = ev ? atoi(ev) : 384;
+    }
+    return v;
+}
+
 // balanced chunks of at most T steps (the complex blocked sweeps instantiate T <= 4)
 static int chunk_cap(int n, int T, int i) {
     const int nc = (n + T - 1) / T;
@@ -790,7 +800,7 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     // latency-bound, 48 us per 4-step launch at 31^2 against 4 x 6.4 us for
     // the one-step kernel; measured break-even between 255^2 and 511^2)
     const bool cblocked9 = !blocked && A->var9h && s->precond == RG_PRECOND_NONE &&
-                           block_T != 1 && (block_T > 1 || A->d.side >= 384);
+                           block_T != 1 && (block_T > 1 || A->d.side >= cb9_min_side());
     std::vector<double> hscale;
     const bool jac = s->precond == RG_PRECOND_JACOBI_SCALAR;
     if (blocked && jac) {

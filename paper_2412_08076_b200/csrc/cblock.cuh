@@ -206,6 +206,20 @@ namespace rg {
 // (kernel parameters), the others read their 9 planes (L1/L2).  CSR column
 // order (-1,-1),(-1,0),(-1,1),(0,-1),(0,0),(0,1),(1,-1),(1,0),(1,1),
 // unfused complex products: bitwise the CSR matvec (apply_op<VAR9>).
+
+#ifndef CB9_LR
+#define CB9_LR 32
+#endif
+#ifndef CB9_MINB
+#define CB9_MINB 2
+#endif
+__host__ __device__ inline int cblock9_ntiles(int side, int T, int* nty) {
+    const int TX = CB9_LR - 2 * T, TY = CB_LC - 2 * T;
+    const int ny = (side + TY - 1) / TY;
+    if (nty) *nty = ny;
+    return ((side + TX - 1) / TX) * ny;
+}
+
 struct CBlock9Args {
     double2 c9[9];
     const double2* planes;        // [9][P] (one coefficient set, shared by the batch)
@@ -225,9 +239,9 @@ struct CBlock9Args {
 };
 
 template <int VAR, int T>
-__global__ void __launch_bounds__(CB_NW * 32, 2) cblock9_kernel(const __grid_constant__ CBlock9Args a) {
+__global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __grid_constant__ CBlock9Args a) {
     typedef double2 C;
-    constexpr int LR = CB_LR, LC = CB_LC;
+    constexpr int LR = CB9_LR, LC = CB_LC;
     constexpr int RPW = LR / CB_NW, CPT = LC / 32;
     constexpr int TX = LR - 2 * T, TY = LC - 2 * T;
     constexpr bool NAG = VAR >= V_NAG;
@@ -354,7 +368,7 @@ __global__ void __launch_bounds__(CB_NW * 32, 2) cblock9_kernel(const __grid_con
 template <int VAR, int T>
 cudaError_t launch_cblock9_t(const CBlock9Args& a0, int batch, cudaStream_t st) {
     auto kern = cblock9_kernel<VAR, T>;
-    const size_t smem = 3 * (size_t)CB_LR * CB_LC * sizeof(double2);
+    const size_t smem = 3 * (size_t)CB9_LR * CB_LC * sizeof(double2);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -362,7 +376,7 @@ cudaError_t launch_cblock9_t(const CBlock9Args& a0, int batch, cudaStream_t st) 
         attr_set = true;
     }
     CBlock9Args a = a0;
-    const int nt = cblock_ntiles(a.side, T, &a.nty);
+    const int nt = cblock9_ntiles(a.side, T, &a.nty);
     kern<<<dim3(nt, batch), dim3(CB_NW * 32), smem, st>>>(a);
     return cudaGetLastError();
 }
