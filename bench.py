@@ -335,7 +335,10 @@ def run_gpu(args, rank, world, local):
         cpu = None
         if world == 1 and not args.no_cpu:
             ref = CpuReference()
-            k_inner = 16
+            # bounded sample of ~10 s wall: a short probe sizes the real run
+            k_probe = 4
+            tp = ref.run(k_probe)
+            k_inner = max(k_probe, int(np.ceil(k_probe * args.cpu_seconds / max(tp, 1e-3))))
             tc = ref.run(k_inner)
             cpu = {"value": ref.updates(k_inner) / tc, "unit": UNIT, "cores": ref.cores,
                    "kind": "port",
@@ -400,6 +403,8 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=2)
     ap.add_argument("--no-time-to-tol", dest="time_to_tol", action="store_false")  # kept for scripts
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", dest="cpu_seconds", type=float, default=10.0,
+                    help="wall-time target of the bounded CPU baseline sample")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
