@@ -162,6 +162,16 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
             if (NAG && a.norm_first_u) buf1[r0 + rr][col] = u;
         }
     }
+    // the T steps' weights, loaded once (a global load after every step's
+    // barrier would stall all warps on L2 latency together)
+    __shared__ double sw[3][8];
+    if (threadIdx.x < T) {
+        const int k = a.k0 + threadIdx.x;
+        const int si = b * a.m + (k % a.m);
+        sw[0][threadIdx.x] = a.omega[si];
+        sw[1][threadIdx.x] = HASV ? a.alpha[si] : 0.0;
+        sw[2][threadIdx.x] = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+    }
     __syncthreads();
 
     double acc[NACC];
@@ -243,11 +253,9 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
         constexpr bool INTERIOR = decltype(interior)::value;
 #pragma unroll
         for (int t = 0; t < T; ++t) {
-            const int k = a.k0 + t;
-            const int si = b * a.m + (k % a.m);
-            const double w = a.omega[si];
-            const double al = HASV ? a.alpha[si] : 0.0;
-            const double atn = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+            const double w = sw[0][t];
+            const double al = sw[1][t];
+            const double atn = sw[2][t];
             Row* cur = (t & 1) ? buf1 : buf0;
             Row* nxt = (t & 1) ? buf0 : buf1;
             const bool last = (t == T - 1);

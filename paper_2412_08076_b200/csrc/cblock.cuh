@@ -101,15 +101,22 @@ __global__ void __launch_bounds__(CB_NW * 32, CB_MINB) cblock_kernel(const __gri
             buf0[r0 + rr][col] = (NAG && in) ? add(u, rmul(at0, v)) : u;   // (:119)
         }
     }
+    // the T steps' weights, loaded once (see block.cuh)
+    __shared__ double sw[3][8];
+    if (threadIdx.x < T) {
+        const int k = a.k0 + threadIdx.x;
+        const int si = b * a.m + (k % a.m);
+        sw[0][threadIdx.x] = a.omega[si];
+        sw[1][threadIdx.x] = HASV ? a.alpha[si] : 0.0;
+        sw[2][threadIdx.x] = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+    }
     __syncthreads();
 
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-        const int k = a.k0 + t;
-        const int si = b * a.m + (k % a.m);
-        const double w = a.omega[si];
-        const double al = HASV ? a.alpha[si] : 0.0;
-        const double atn = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+        const double w = sw[0][t];
+        const double al = sw[1][t];
+        const double atn = sw[2][t];
         Row* cur = (t & 1) ? buf1 : buf0;
         Row* nxt = (t & 1) ? buf0 : buf1;
         const bool last = (t == T - 1);
@@ -283,15 +290,22 @@ __global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __g
             buf0[r0 + rr][col] = (NAG && in) ? add(u, rmul(at0, v)) : u;
         }
     }
+    // the T steps' weights, loaded once (see block.cuh)
+    __shared__ double sw[3][8];
+    if (threadIdx.x < T) {
+        const int k = a.k0 + threadIdx.x;
+        const int si = b * a.m + (k % a.m);
+        sw[0][threadIdx.x] = a.omega[si];
+        sw[1][threadIdx.x] = HASV ? a.alpha[si] : 0.0;
+        sw[2][threadIdx.x] = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+    }
     __syncthreads();
 
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-        const int k = a.k0 + t;
-        const int si = b * a.m + (k % a.m);
-        const double w = a.omega[si];
-        const double al = HASV ? a.alpha[si] : 0.0;
-        const double atn = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+        const double w = sw[0][t];
+        const double al = sw[1][t];
+        const double atn = sw[2][t];
         Row* cur = (t & 1) ? buf1 : buf0;
         Row* nxt = (t & 1) ? buf0 : buf1;
         const bool last = (t == T - 1);

@@ -89,6 +89,17 @@ __device__ __forceinline__ bool finite(float x)   { return isfinite(x); }
 __device__ __forceinline__ bool finite(double x)  { return isfinite(x); }
 __device__ __forceinline__ bool finite(double2 x) { return isfinite(x.x) && isfinite(x.y); }
 
+// ---- asynchronous global -> shared element copies (zero-filled when !valid)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_el(void* sdst, const void* gsrc, bool valid) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(sa), "l"(gsrc), "n"(BYTES),
+                 "r"(valid ? BYTES : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // ---- per-system solver state (device) ------------------------------------
 // Mirrors the local variables of solve_stationary (richardson.py:92-136).
 struct SysState {

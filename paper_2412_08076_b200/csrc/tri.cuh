@@ -66,15 +66,6 @@ struct TriArgs {
 // from SuperLU's, agreement ~1e-15, inside the reference's 1e-13 bar.
 constexpr int TRI_WS = TRI_PF + 1;   // padded row stride of the staging buffers
 
-template <int BYTES>
-__device__ __forceinline__ void cp_async_el(void* sdst, const void* gsrc, bool valid) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(sa), "l"(gsrc), "n"(BYTES),
-                 "r"(valid ? BYTES : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 template <bool REV, bool MULD, bool SCALE, typename SI, typename SO>
 __device__ __forceinline__ void tri_sweep(const SI* __restrict__ src, SO* __restrict__ dst, int side,
