@@ -286,15 +286,22 @@ static int dst_pass(const rg_dst* D, int axis, int mode, const double* in, doubl
     a.lpc = D->lpc;
     a.mode = mode;
     a.scale = sqrt(2.0 / D->M);
-    const size_t smem = 2 * (size_t)D->lpc * D->M * sizeof(double2);   // Stockham ping-pong
+    // in-place FFT: lpc lines + the twiddle table (M <= DST_SMEM_TW_MAX)
+    const size_t smem = ((size_t)D->lpc * dst_ls(D->M) + (D->M <= DST_SMEM_TW_MAX ? D->M : 0)) * sizeof(double2) +
+                        (mode == DST_TWICE_LAM ? (size_t)D->lpc * (D->M + 8) * sizeof(double) : 0);   // lam staging
+    const int nt = D->lpc * (D->M / dst_vpt(D->M));
     const dim3 grid((D->side + D->lpc - 1) / D->lpc, D->batch);
-    if (axis == 0) {
-        CUDA_TRY(cudaFuncSetAttribute(dst_lines_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dst_lines_kernel<0><<<grid, DST_NT, smem, st>>>(a);
-    } else {
-        CUDA_TRY(cudaFuncSetAttribute(dst_lines_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dst_lines_kernel<1><<<grid, DST_NT, smem, st>>>(a);
-    }
+    auto go = [&](auto kern) -> int {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, nt, smem, st>>>(a);
+        return RG_OK;
+    };
+    int rc;
+    if (D->M == 1024 && D->lpc == DST_FIXED_LPC)   // cfg4's size: compile-time indexing
+        rc = axis == 0 ? go(dst_lines_kernel<0, 256, 10>) : go(dst_lines_kernel<1, 256, 10>);
+    else if (nt <= 256) rc = axis == 0 ? go(dst_lines_kernel<0, 256, 0>) : go(dst_lines_kernel<1, 256, 0>);
+    else rc = axis == 0 ? go(dst_lines_kernel<0, 512, 0>) : go(dst_lines_kernel<1, 512, 0>);
+    if (rc) return rc;
     LAUNCH_CHECK();
     return RG_OK;
 }
@@ -971,10 +978,14 @@ int rg_dst_create(rg_dst** out, int batch, int side) {
     D->M = M;
     D->logM = 0;
     while ((1 << D->logM) < M) ++D->logM;
-    int lpc = 1024 / M;   // 2 x lpc x M x 16 B of shared memory per CTA (1 line of 1023:
-                          // 7 CTAs/SM; 2 lines measured 6% slower per FNS alternation)
-    if (const char* ev = getenv("RG_DST_POINTS")) lpc = atoi(ev) / M;   // tuning override
-    D->lpc = lpc < 1 ? 1 : (lpc > 8 ? 8 : lpc);
+    // lines per CTA: <= 256 threads (M / dst_vpt(M) per line; 512 for M = 8192)
+    const int tpl = M / dst_vpt(M);
+    int lpc = 256 / tpl;
+    if (const char* ev = getenv("RG_DST_LPC")) lpc = atoi(ev);   // tuning override
+    if (lpc * tpl > 256) lpc = 256 / tpl;
+    if (lpc < 1) lpc = 1;
+    while (lpc & (lpc - 1)) lpc &= lpc - 1;   // a power of two (index shifts in the kernel)
+    D->lpc = lpc;
     std::vector<double2> tw(M);
     for (int k = 0; k < M; ++k) {
         // (cos, sin)(pi k / M), symmetric evaluation for accuracy
