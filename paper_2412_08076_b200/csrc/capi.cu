@@ -273,8 +273,22 @@ struct rg_dst {
     double* work;    // [batch][side][side] residual / intermediate
 };
 
+// Lines per CTA of the compile-time M = 1024 kernels (cfg4's size), per axis;
+// RG_DST_LPC_ROW / RG_DST_LPC_COL (2 or 4) override for tuning.
+static int dst_lpc_1024(int axis) {
+    static int v[2] = {-1, -1};
+    if (v[axis] < 0) {
+        const char* ev = getenv(axis == 0 ? "RG_DST_LPC_ROW" : "RG_DST_LPC_COL");
+        v[axis] = ev ? atoi(ev) : 4;   // measured: 4 / 4 best (0.380 ms per FNS alternation)
+        if (v[axis] != 2) v[axis] = 4;
+    }
+    return v[axis];
+}
+
 static int dst_pass(const rg_dst* D, int axis, int mode, const double* in, double* out,
                     const double* lam, cudaStream_t st) {
+    const bool cm = D->M == 1024;   // compile-time indexing
+    const int lpc = cm ? dst_lpc_1024(axis) : D->lpc;
     DstArgs a;
     a.in = in;
     a.out = out;
@@ -283,24 +297,24 @@ static int dst_pass(const rg_dst* D, int axis, int mode, const double* in, doubl
     a.N = D->side;
     a.M = D->M;
     a.logM = D->logM;
-    a.lpc = D->lpc;
+    a.lpc = lpc;
     a.mode = mode;
     a.scale = sqrt(2.0 / D->M);
-    // in-place FFT: lpc lines + the twiddle table (M <= DST_SMEM_TW_MAX)
-    const size_t smem = ((size_t)D->lpc * dst_ls(D->M) + (D->M <= DST_SMEM_TW_MAX ? D->M : 0)) * sizeof(double2) +
-                        (mode == DST_TWICE_LAM ? (size_t)D->lpc * (D->M + 8) * sizeof(double) : 0);   // lam staging
-    const int nt = D->lpc * (D->M / dst_vpt(D->M));
-    const dim3 grid((D->side + D->lpc - 1) / D->lpc, D->batch);
+    // in-place FFT: lpc lines + the twiddle table (M <= DST_SMEM_TW_MAX) + lam staging
+    const size_t smem = ((size_t)lpc * dst_ls(D->M) + (D->M <= DST_SMEM_TW_MAX ? D->M : 0)) * sizeof(double2) +
+                        (mode == DST_TWICE_LAM ? (size_t)lpc * (D->M + 8) * sizeof(double) : 0);
+    const int nt = lpc * (D->M / dst_vpt(D->M));
+    const dim3 grid((D->side + lpc - 1) / lpc, D->batch);
     auto go = [&](auto kern) -> int {
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<grid, nt, smem, st>>>(a);
         return RG_OK;
     };
     int rc;
-    if (D->M == 1024 && D->lpc == DST_FIXED_LPC)   // cfg4's size: compile-time indexing
-        rc = axis == 0 ? go(dst_lines_kernel<0, 256, 10>) : go(dst_lines_kernel<1, 256, 10>);
-    else if (nt <= 256) rc = axis == 0 ? go(dst_lines_kernel<0, 256, 0>) : go(dst_lines_kernel<1, 256, 0>);
-    else rc = axis == 0 ? go(dst_lines_kernel<0, 512, 0>) : go(dst_lines_kernel<1, 512, 0>);
+    if (cm && lpc == 2) rc = axis == 0 ? go(dst_lines_kernel<0, 256, 10, 2>) : go(dst_lines_kernel<1, 256, 10, 2>);
+    else if (cm) rc = axis == 0 ? go(dst_lines_kernel<0, 256, 10, 4>) : go(dst_lines_kernel<1, 256, 10, 4>);
+    else if (nt <= 256) rc = axis == 0 ? go(dst_lines_kernel<0, 256, 0, 0>) : go(dst_lines_kernel<1, 256, 0, 0>);
+    else rc = axis == 0 ? go(dst_lines_kernel<0, 512, 0, 0>) : go(dst_lines_kernel<1, 512, 0, 0>);
     if (rc) return rc;
     LAUNCH_CHECK();
     return RG_OK;
@@ -1033,8 +1047,8 @@ int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u
     memset(&q, 0, sizeof q);
     q.u_in = u;
     q.f = f;
-    q.r_out = D->work;   // r = f - A u
-    q.m = 1;
+    q.r_out = D->work;   // r = f - A u  (a separate pass: measured faster than
+    q.m = 1;             // recomputing the stencil inside the row transform's load)
     if ((rc = step1(A, q, st))) return rc;
     if ((rc = dst_pass(D, 0, DST_PLAIN, D->work, D->work, nullptr, st))) return rc;
     if ((rc = dst_pass(D, 1, DST_TWICE_LAM, D->work, D->work, lam, st))) return rc;

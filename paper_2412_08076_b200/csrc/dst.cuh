@@ -274,20 +274,18 @@ constexpr int DST_SMEM_TW_MAX = 2048;
 // CTA, lpc * M / dst_vpt(M) <= MAXNT threads, shared memory lpc * M complex
 // values (+ the twiddle table for M <= DST_SMEM_TW_MAX); 128 registers per
 // thread for the 16 in-flight complex values (2 CTAs/SM at MAXNT = 256).
-// LOGM > 0: compile-time M = 2^LOGM and lpc = DST_FIXED_LPC (all index
-// arithmetic folds to constants); LOGM = 0: runtime M, lpc.
-constexpr int DST_FIXED_LPC = 4;
-template <int AXIS, int MAXNT, int LOGM>
+// LOGM > 0: compile-time M = 2^LOGM and lpc = LPC (all index arithmetic
+// folds to constants); LOGM = 0: runtime M, lpc.
+template <int AXIS, int MAXNT, int LOGM, int LPC>
 __global__ void __launch_bounds__(MAXNT, 512 / MAXNT) dst_lines_kernel(DstArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr bool CM = LOGM > 0;
     const int M = CM ? (1 << LOGM) : a.M;
     const int N = M - 1;
-    const int lpc = CM ? DST_FIXED_LPC : a.lpc;          // a power of two
+    const int lpc = CM ? LPC : a.lpc;                    // a power of two
     const int logM = CM ? LOGM : a.logM;
-    const int llp = CM ? (DST_FIXED_LPC == 1 ? 0 : DST_FIXED_LPC == 2 ? 1 : DST_FIXED_LPC == 4 ? 2 : 3)
-                       : __ffs(lpc) - 1;
-    const int nt = CM ? (DST_FIXED_LPC << LOGM) / 16 : (int)blockDim.x;
+    const int llp = CM ? (LPC == 1 ? 0 : LPC == 2 ? 1 : LPC == 4 ? 2 : 3) : __ffs(lpc) - 1;
+    const int nt = CM ? (LPC << LOGM) / 16 : (int)blockDim.x;
     double2* z = reinterpret_cast<double2*>(smem_raw);
     double2* tws = z + lpc * dst_ls(M);
     const bool tw_sm = CM || M <= DST_SMEM_TW_MAX;      // (CM sizes are <= DST_SMEM_TW_MAX)
