@@ -378,6 +378,18 @@ static int chunk_len(int n, int T, int i) {
     return 1;
 }
 
+// largest grid (unknowns per system) swept by the single-launch cluster
+// kernel (psweep.cuh); RG_PS_MAX overrides for tuning
+static size_t ps_max_unknowns() {
+    static long v = -1;
+    if (v < 0) {
+        const char* ev = getenv("RG_PS_MAX");
+        v = ev ? atol(ev) : 16 * PS_NT_BIG;
+        if (v > 16 * PS_NT_BIG) v = 16 * PS_NT_BIG;
+    }
+    return (size_t)v;
+}
+
 // smallest side that takes the blocked 9-point complex sweep automatically
 static int cb9_min_side() {
     static int v = -1;
@@ -836,11 +848,11 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     const int TC = block_T == 0 ? 4 : (block_T < 4 ? block_T : 4);
     // small grids (coarse V-cycle levels): every step in one cooperative launch
     const size_t total = (size_t)A->d.batch * A->P;
-    // (one point per thread: a 16-CTA cluster covers 4096 unknowns; at 127^2,
-    // 4 points per thread, the cluster sweep measured slower than 16
-    // one-step launches: 129 vs 102 us)
+    // (one point per thread: a 16-CTA cluster of 1024-thread CTAs covers
+    // 16384 unknowns; with 256-thread CTAs and 4 points per thread, 127^2
+    // measured slower than 16 one-step launches: 129 vs 102 us)
     bool small = !blocked && !cblocked && !cblocked9 && block_T == 0 && n_steps >= 2 &&
-                 (A->d.dtype == RG_F64 || A->d.dtype == RG_C128) && A->P <= 16 * PS_NT;
+                 (A->d.dtype == RG_F64 || A->d.dtype == RG_C128) && A->P <= ps_max_unknowns();
     if (small && !A->ps_ws) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
         cudaStreamIsCapturing(st, &cs);

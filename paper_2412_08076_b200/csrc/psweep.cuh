@@ -10,15 +10,17 @@
 // or the NAG look-ahead u + at v) ping-pongs through two L2-resident
 // buffers, u and v are updated in place (pointwise), f and the
 // coefficients stay in L2.  The arithmetic is step1_kernel's, operation for
-// operation (bitwise).  Used up to 4096 unknowns per system (one point per
-// thread); 16 smoothing steps at 63^2 take 50 us against 102 us.
+// operation (bitwise).  One point per thread: 256-thread CTAs up to 4096
+// unknowns per system, 1024-thread CTAs up to 16384 (127^2); 16 smoothing
+// steps at 63^2 take 50 us against 102 us.
 #pragma once
 #include <cooperative_groups.h>
 #include "step.cuh"
 
 namespace rg {
 
-constexpr int PS_NT = 256;
+constexpr int PS_NT = 256;        // threads per CTA up to 16 * 256 unknowns
+constexpr int PS_NT_BIG = 1024;   // up to 16 * 1024 (127^2): still one point per thread
 
 template <typename S>
 struct PsArgs {
@@ -36,8 +38,8 @@ struct PsArgs {
     int m, k0, n_steps, B;
 };
 
-template <typename S, int KIND, int VAR>
-__global__ void __launch_bounds__(PS_NT) psweep_kernel(const __grid_constant__ PsArgs<S> a) {
+template <typename S, int KIND, int VAR, int NT>
+__global__ void __launch_bounds__(NT) psweep_kernel(const __grid_constant__ PsArgs<S> a) {
     typedef CT<S> C;
     constexpr bool NAG = VAR >= V_NAG;
     constexpr bool HASV = VAR != V_PLAIN;
@@ -92,20 +94,20 @@ __global__ void __launch_bounds__(PS_NT) psweep_kernel(const __grid_constant__ P
     }
 }
 
-template <typename S, int KIND, int VAR>
-cudaError_t launch_psweep_t(const PsArgs<S>& a, cudaStream_t st) {
-    auto kern = psweep_kernel<S, KIND, VAR>;
+template <typename S, int KIND, int VAR, int NT>
+cudaError_t launch_psweep_n(const PsArgs<S>& a, cudaStream_t st) {
+    auto kern = psweep_kernel<S, KIND, VAR, NT>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    int cs = (int)((a.A.P + PS_NT - 1) / PS_NT);
+    int cs = (int)((a.A.P + NT - 1) / NT);
     cs = cs < 1 ? 1 : (cs > 16 ? 16 : cs);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.B * cs);
-    cfg.blockDim = dim3(PS_NT);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -116,6 +118,12 @@ cudaError_t launch_psweep_t(const PsArgs<S>& a, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <typename S, int KIND, int VAR>
+cudaError_t launch_psweep_t(const PsArgs<S>& a, cudaStream_t st) {
+    return a.A.P <= 16 * PS_NT ? launch_psweep_n<S, KIND, VAR, PS_NT>(a, st)
+                               : launch_psweep_n<S, KIND, VAR, PS_NT_BIG>(a, st);
 }
 
 template <typename S, int KIND>
