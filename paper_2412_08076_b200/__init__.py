@@ -18,6 +18,12 @@ from .richardson import (StationarySolver, inner_update, outer_sweep, solve_stat
                          solve_stationary_batched)
 from .schedules import (WeightSchedule, chebyshev_semi_weights, chebyshev_weights, leja_order,
                         stencil_symbol_bounds)
+# the reference's top-level names for the rest of the path (richlab/__init__.py:4-31)
+from .fns import SpectralCorrection, dst2, dst2_inv, fns_lite_step, solve_fns
+from .multigrid import (build_hierarchy, prolongation_matrix, restriction_matrix,
+                        v_cycle)
+from .fgmres import FgmresConfig, fgmres
+from .spectral import SpectralBounds, estimate_lambda_max, estimate_lambda_min
 
 __version__ = "0.1.0"
 __all__ = [n for n in dir() if not n.startswith("_")]
