@@ -30,7 +30,8 @@ sys.path.insert(0, str(ROOT))
 import oracle as O  # noqa: E402  (checker + CPU baseline only)
 import paper_2412_08076_b200 as G  # noqa: E402
 from paper_2412_08076_b200 import configs as CF  # noqa: E402
-from paper_2412_08076_b200 import fgmres as GG  # noqa: E402
+import paper_2412_08076_b200.fgmres  # noqa: E402,F401  (the package attribute is the function)
+GG = sys.modules["paper_2412_08076_b200.fgmres"]
 from paper_2412_08076_b200 import fns as GF  # noqa: E402
 from paper_2412_08076_b200 import multigrid as GM  # noqa: E402
 

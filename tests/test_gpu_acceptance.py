@@ -3,12 +3,15 @@
 (criterion 4), the unroll gradient against central differences (5), the
 exact spectral correction (6), V-cycle residual non-increase (7) and the
 V-cycle-preconditioned FGMRES on Helmholtz (8)."""
+import sys
+
 import numpy as np
 import pytest
 
 import oracle as O
 import paper_2412_08076_b200 as G
-from paper_2412_08076_b200 import fgmres as GG
+import paper_2412_08076_b200.fgmres  # noqa: E402,F401  (the package attribute is the function)
+GG = sys.modules["paper_2412_08076_b200.fgmres"]
 from paper_2412_08076_b200 import fns as GF
 from paper_2412_08076_b200 import multigrid as GM
 from paper_2412_08076_b200 import training as T
