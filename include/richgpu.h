@@ -147,7 +147,8 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
 
 /* ---- DST-I / FNS correction (transforms.py:24-35, fns.py:30-84) ----------
  * A plan holds the twiddle table and one [batch][side][side] workspace; one
- * call in flight per plan.  side+1 must be a power of two (4 .. 8192). */
+ * call in flight per plan.  side+1 a power of two (4 .. 8192): FFT path;
+ * any other side <= 4096: dense orthonormal sine-matrix products. */
 typedef struct rg_dst rg_dst;
 int rg_dst_create(rg_dst** out, int batch, int side);
 int rg_dst_destroy(rg_dst* plan);

@@ -271,7 +271,28 @@ struct rg_dst {
     int batch, side, M, logM, lpc;
     double2* tw;     // [M]
     double* work;    // [batch][side][side] residual / intermediate
+    // dense path (side + 1 not a power of two): the orthonormal DST-I matrix
+    bool dense = false;
+    double* S = nullptr;      // [side][side]
+    double* work2 = nullptr;  // [batch][side][side]
 };
+
+// C = P Q for every system (dense DST path); P or Q may be the shared S.
+static int dst_gemm(const rg_dst* D, const double* P, bool p_batched, const double* Q,
+                    bool q_batched, double* C, int mode, const double* lam, cudaStream_t st) {
+    GemmArgs g;
+    const size_t NN = (size_t)D->side * D->side;
+    g.P = P; g.sP = p_batched ? NN : 0;
+    g.Q = Q; g.sQ = q_batched ? NN : 0;
+    g.C = C; g.sC = NN;
+    g.lam = lam;
+    g.N = D->side;
+    g.mode = mode;
+    const int nb = (D->side + GM_T - 1) / GM_T;
+    dst_gemm_kernel<<<dim3(nb, nb, D->batch), GM_NT, 0, st>>>(g);
+    LAUNCH_CHECK();
+    return RG_OK;
+}
 
 // Lines per CTA of the compile-time M = 1024 kernels (cfg4's size), per axis;
 // RG_DST_LPC_ROW / RG_DST_LPC_COL (2 or 4) override for tuning.
@@ -996,8 +1017,38 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
 int rg_dst_create(rg_dst** out, int batch, int side) {
     if (!out) return fail(RG_ENULL, "null out");
     const int M = side + 1;
-    if (batch < 1 || side < 3 || (M & (M - 1)) != 0 || M > 8192)
-        return fail(RG_EUNSUPPORTED, "DST needs side+1 a power of two in [4, 8192] (got side=%d)", side);
+    if (batch < 1 || side < 1) return fail(RG_EINVAL, "DST needs batch >= 1 and side >= 1");
+    if ((M & (M - 1)) != 0 || M < 4 || M > 8192) {
+        // any other size: dense sine-matrix products (S X S)
+        if (side > 4096) return fail(RG_EUNSUPPORTED, "DST side %d: not a power of two minus one, "
+                                     "and above the dense path's 4096", side);
+        rg_dst* D = new rg_dst();
+        D->batch = batch;
+        D->side = side;
+        D->M = M;
+        D->dense = true;
+        const size_t NN = (size_t)side * side;
+        std::vector<double> S(NN);
+        const double sc = sqrt(2.0 / M);
+        for (int j = 0; j < side; ++j)
+            for (int k = 0; k < side; ++k) {
+                const long long a = ((long long)(j + 1) * (k + 1)) % (2LL * M);   // sin is 2M-periodic in a
+                S[(size_t)j * side + k] = sc * sin(M_PI * (double)a / (double)M);
+            }
+        cudaError_t e;
+        if ((e = cudaMalloc((void**)&D->S, sizeof(double) * NN)) != cudaSuccess ||
+            (e = cudaMalloc((void**)&D->work, sizeof(double) * batch * NN)) != cudaSuccess ||
+            (e = cudaMalloc((void**)&D->work2, sizeof(double) * batch * NN)) != cudaSuccess ||
+            (e = cudaMemcpy(D->S, S.data(), sizeof(double) * NN, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            cudaFree(D->S);
+            cudaFree(D->work);
+            cudaFree(D->work2);
+            delete D;
+            return fail(RG_ECUDA, "dst plan: %s", cudaGetErrorString(e));
+        }
+        *out = D;
+        return RG_OK;
+    }
     rg_dst* D = new rg_dst();
     D->batch = batch;
     D->side = side;
@@ -1035,6 +1086,8 @@ int rg_dst_destroy(rg_dst* D) {
     if (!D) return RG_OK;
     cudaFree(D->tw);
     cudaFree(D->work);
+    cudaFree(D->S);
+    cudaFree(D->work2);
     delete D;
     return RG_OK;
 }
@@ -1042,6 +1095,11 @@ int rg_dst_destroy(rg_dst* D) {
 int rg_dst2(const rg_dst* D, const double* in, double* out, void* stream) {
     if (!D || !in || !out) return fail(RG_ENULL, "null argument");
     cudaStream_t st = (cudaStream_t)stream;
+    if (D->dense) {   // out = S (in S)
+        int rc = dst_gemm(D, in, true, D->S, false, D->work2, GEMM_STORE, nullptr, st);
+        if (rc) return rc;
+        return dst_gemm(D, D->S, false, D->work2, true, out, GEMM_STORE, nullptr, st);
+    }
     int rc = dst_pass(D, 0, DST_PLAIN, in, out, nullptr, st);
     if (rc) return rc;
     return dst_pass(D, 1, DST_PLAIN, out, out, nullptr, st);
@@ -1062,6 +1120,12 @@ int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u
     q.r_out = D->work;   // r = f - A u  (a separate pass: measured faster than
     q.m = 1;             // recomputing the stencil inside the row transform's load)
     if ((rc = step1(A, q, st))) return rc;
+    if (D->dense) {   // u += S ((S (r S)) * lam) S
+        if ((rc = dst_gemm(D, D->work, true, D->S, false, D->work2, GEMM_STORE, nullptr, st))) return rc;
+        if ((rc = dst_gemm(D, D->S, false, D->work2, true, D->work, GEMM_LAM, lam, st))) return rc;
+        if ((rc = dst_gemm(D, D->work, true, D->S, false, D->work2, GEMM_STORE, nullptr, st))) return rc;
+        return dst_gemm(D, D->S, false, D->work2, true, u, GEMM_ADD, nullptr, st);
+    }
     if ((rc = dst_pass(D, 0, DST_PLAIN, D->work, D->work, nullptr, st))) return rc;
     if ((rc = dst_pass(D, 1, DST_TWICE_LAM, D->work, D->work, lam, st))) return rc;
     return dst_pass(D, 0, DST_ADD, D->work, u, nullptr, st);

@@ -379,4 +379,73 @@ __global__ void __launch_bounds__(MAXNT, 512 / MAXNT) dst_lines_kernel(DstArgs a
     }
 }
 
+// ---- dense path for any n (side + 1 not a power of two) -------------------
+// The orthonormal DST-I matrix S[j][k] = sqrt(2/n) sin(pi (j+1)(k+1) / n) is
+// symmetric and involutory, so dst2(X) = S X S on the N x N grid (row
+// transform X S, column transform S X).  One tiled FP64 GEMM kernel, C = P Q
+// per system (P or Q is the shared S: batch stride 0), with the FNS
+// epilogues: store, store * lam, or accumulate into u.  2 N^3 flops per
+// product: a fallback for sizes the FFT path does not take (e.g. N = 1000:
+// ~0.15 ms per product per system), ~1e-15 relative like the FFT.
+enum { GEMM_STORE = 0, GEMM_LAM = 1, GEMM_ADD = 2 };
+constexpr int GM_T = 64, GM_K = 16, GM_NT = 256;   // 64 x 64 tile, 4 x 4 per thread
+
+struct GemmArgs {
+    const double* P; size_t sP;   // [B][N][N] or shared (sP = 0)
+    const double* Q; size_t sQ;
+    double* C; size_t sC;
+    const double* lam;            // GEMM_LAM: [B][N][N]
+    int N, mode;
+};
+
+__global__ void __launch_bounds__(GM_NT) dst_gemm_kernel(const GemmArgs a) {
+    __shared__ double Ps[GM_K][GM_T + 1];   // P tile, transposed (k, row)
+    __shared__ double Qs[GM_K][GM_T + 1];   // Q tile (k, col)
+    const int N = a.N, b = blockIdx.z;
+    const double* P = a.P + b * a.sP;
+    const double* Q = a.Q + b * a.sQ;
+    const int r0 = blockIdx.y * GM_T, c0 = blockIdx.x * GM_T;
+    const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;   // 16 x 16 threads, 4 x 4 outputs each
+    double acc[4][4] = {};
+    for (int k0 = 0; k0 < N; k0 += GM_K) {
+        for (int e = threadIdx.x; e < GM_T * GM_K; e += GM_NT) {
+            const int i = e / GM_K, k = e % GM_K;                 // P rows, coalesced along k
+            const int gr = r0 + i, gk = k0 + k;
+            Ps[k][i] = (gr < N && gk < N) ? P[(size_t)gr * N + gk] : 0.0;
+            const int kk = e / GM_T, j = e % GM_T;                // Q rows, coalesced along cols
+            const int gq = k0 + kk, gc = c0 + j;
+            Qs[kk][j] = (gq < N && gc < N) ? Q[(size_t)gq * N + gc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < GM_K; ++k) {
+            double pr[4], qc[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) pr[i] = Ps[k][tr + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) qc[j] = Qs[k][tc + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(pr[i], qc[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    double* C = a.C + b * a.sC;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gr = r0 + tr + 16 * i;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gc = c0 + tc + 16 * j;
+            if (gr < N && gc < N) {
+                const size_t q = (size_t)gr * N + gc;
+                if (a.mode == GEMM_LAM) C[q] = acc[i][j] * a.lam[b * a.sC + q];
+                else if (a.mode == GEMM_ADD) C[q] = C[q] + acc[i][j];   // u = u + correction
+                else C[q] = acc[i][j];
+            }
+        }
+    }
+}
+
 }  // namespace rg

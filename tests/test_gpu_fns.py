@@ -34,6 +34,32 @@ def test_dst2_vs_scipy_and_involution(side):
     assert abs(np.linalg.norm(y) / np.linalg.norm(x) - 1) <= 1e-13   # orthonormal
 
 
+@pytest.mark.parametrize("side", [1, 2, 5, 9, 14, 99, 300])
+def test_dst2_dense_path_any_size(side):
+    """side + 1 not a power of two: the dense sine-matrix path (the reference's
+    pocketfft dstn takes any size, transforms.py:24-30)."""
+    rng = np.random.default_rng(100 + side)
+    x = rng.standard_normal((3, side * side))
+    y = GF.dst2(x)
+    for b in range(3):
+        assert _rel(y[b], O.dst2(x[b])) <= 1e-13
+    assert _rel(GF.dst2(y), x) <= 1e-13
+
+
+@pytest.mark.parametrize("n", [20, 48])
+def test_fns_step_dense_path(n):
+    """fns_lite_step (fns.py:76-84) on a grid whose DST takes the dense path."""
+    rng = np.random.default_rng(n)
+    A = O.assemble_anisotropic(1e-2, 0.7, n)
+    f = rng.standard_normal(A.shape[0])
+    lam = 0.01 * rng.standard_normal(A.shape[0])
+    w = np.full(4, 0.4)
+    u = GF.fns_lite_step(A, f, np.zeros(A.shape[0]), G.WeightSchedule(omega=w), 4,
+                         GF.SpectralCorrection(lam, n))
+    uo = O.fns_lite_step(A, f, np.zeros(A.shape[0]), w, 4, lam)
+    assert _rel(u, uo) <= RTOL
+
+
 def test_sine_mode_is_unit_coefficient():
     """transforms.py:38-43 / test_transforms.py analogue."""
     n = 32
