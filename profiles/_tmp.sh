@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests -m gpu -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$? > gpurun_out/t.log
+python profiles/vcycle_levels.py > gpurun_out/vc.log 2>&1
+RG_CB9_MINSIDE=200 python profiles/vcycle_levels.py >> gpurun_out/vc.log 2>&1
+RG_CB9_MINSIDE=100 python profiles/vcycle_levels.py >> gpurun_out/vc.log 2>&1
