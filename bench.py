@@ -46,6 +46,7 @@ N_SIDE = 1024            # cells per side -> 1023^2 unknowns
 SYSTEMS_PER_GPU = 8
 M = 32
 BYTES_PER_UPDATE = 24    # plain Richardson f64: read u, f; write u
+FP64_PER_POINT_STEP = 22  # blocked kernel SASS: 11 DMUL + 10 DADD + 1 DFMA per point-step
 TOL = 1e-6
 MAX_OUTER_TOL = 10_000
 
@@ -298,6 +299,19 @@ def run_gpu(args, rank, world, local):
     achieved = float(BYTES_PER_UPDATE * B * Pn * steps_l.sum() / dur.sum() / 1e9)
     peak = _peak_hbm()
     share = float(dur.sum() / t_local)
+    # the bound that actually limits the blocked kernel: FP64 issue.  Every
+    # launch computes its whole 64 x 64 windows (owned points + T-cell halo)
+    # T times, 22 FP64 instructions per point-step (11 DMUL + 10 DADD + 1
+    # DFMA: the reference's unfused CSR-order sum, SASS-counted).
+    side = N_SIDE - 1
+    computed = 0.0
+    for T_, d_ in zip(steps_l, dur):
+        T_ = int(T_)
+        tiles = (-(-side // (64 - 2 * T_))) ** 2   # block_ntiles: ceil(side / (64 - 2T))^2
+        computed += tiles * 64 * 64 * T_ * B
+    fp64_rate = computed * FP64_PER_POINT_STEP / float(dur.sum())
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp64_peak = n_sm * 64 * (clk.summary().get("sm_mhz") or 1965.0) * 1e6
 
     # ---- end to end through the public API: one e2e step is the call a
     # richlab user makes, solve_stationary(..., tol=1e-6), batched over the
@@ -367,7 +381,16 @@ def run_gpu(args, rank, world, local):
                             "avg_launch_s": avg, "kernel_share_of_step": share,
                             "note": "algorithmic bytes count 24 B per point-update per inner "
                                     "step; temporal blocking fuses T steps per HBM pass, so "
-                                    "frac can exceed 1 (SURVEY.md §8(d))"},
+                                    "frac can exceed 1 (SURVEY.md §8(d))",
+                            "fp64_issue": {"achieved_Tinst_s": fp64_rate / 1e12,
+                                           "peak_Tinst_s": fp64_peak / 1e12,
+                                           "frac": fp64_rate / fp64_peak,
+                                           "computed_point_steps_per_owned": computed / (
+                                               B * Pn * float(steps_l.sum())),
+                                           "note": "FP64 instructions issued (22 per computed "
+                                                   "point-step, halo recomputation included) "
+                                                   "against SMs x 64 FP64 lanes x SM clock: "
+                                                   "the limiting pipe of the blocked kernel"}},
                "cpu_baseline": cpu, "time_to_tol": ttt}
     return out
 

@@ -67,6 +67,9 @@ struct BlockArgs {
 #ifndef RG_BLK_NW
 #define RG_BLK_NW 8
 #endif
+#ifndef RG_BLK_LC
+#define RG_BLK_LC 64
+#endif
 
 // Occupancy target per (scalar, variant): registers hold f (+v, +u for nag).
 #ifndef RG_MINB_PLAIN_F64
@@ -75,12 +78,12 @@ struct BlockArgs {
 // (f32 storage computes in f64, so the register budget does not depend on S)
 template <typename S, int VAR>
 struct BlockMinCtas {
-    static constexpr int value = (RG_BLK_LR * 64 * 16 > 100 * 1024) ? 1
+    static constexpr int value = (RG_BLK_LR * RG_BLK_LC * 16 > 100 * 1024) ? 1
                                  : ((VAR == V_PLAIN) ? RG_MINB_PLAIN_F64 : 2);
 };
 
 // Tile shape used by the library (load window LR x LC, NW warps).
-constexpr int BLK_LR = RG_BLK_LR, BLK_LC = 64, BLK_NW = RG_BLK_NW;
+constexpr int BLK_LR = RG_BLK_LR, BLK_LC = RG_BLK_LC, BLK_NW = RG_BLK_NW;
 
 __host__ __device__ inline int block_ntiles(int side, int T, int* nty) {
     const int TX = BLK_LR - 2 * T, TY = BLK_LC - 2 * T;
