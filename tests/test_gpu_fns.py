@@ -34,6 +34,26 @@ def test_dst2_vs_scipy_and_involution(side):
     assert abs(np.linalg.norm(y) / np.linalg.norm(x) - 1) <= 1e-13   # orthonormal
 
 
+@pytest.mark.parametrize("side", [2047, 4095])
+def test_dst2_large_fft_sizes(side):
+    """M = 2048 (shared twiddles, 2 lines per CTA) and M = 4096 (global
+    twiddle table, one line per CTA) against scipy's dstn."""
+    x = np.random.default_rng(side).standard_normal(side * side)
+    y = GF.dst2(x)
+    assert _rel(y, O.dst2(x)) <= 1e-13
+
+
+def test_dst2_largest_fft_size_properties():
+    """M = 8192 (512-thread CTAs): involutory and orthonormal (no oracle call:
+    size-independent properties, transforms.py:33-35)."""
+    side = 8191
+    x = torch.randn(side * side, dtype=torch.float64, device="cuda",
+                    generator=torch.Generator(device="cuda").manual_seed(1))
+    y = GF.dst2(x)
+    assert abs(float(torch.linalg.norm(y) / torch.linalg.norm(x)) - 1) <= 1e-13
+    assert float(torch.linalg.norm(GF.dst2(y) - x) / torch.linalg.norm(x)) <= 1e-13
+
+
 @pytest.mark.parametrize("side", [1, 2, 5, 9, 14, 99, 300])
 def test_dst2_dense_path_any_size(side):
     """side + 1 not a power of two: the dense sine-matrix path (the reference's
