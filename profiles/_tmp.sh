@@ -1,3 +1,2 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$? > gpurun_out/c1.log
-python profiles/cfg1_probe.py >> gpurun_out/c1.log 2>&1
+python -m pytest tests/test_gpu_parity.py -q -k "above_64" > gpurun_out/t.log 2>&1; echo rc=$? >> gpurun_out/t.log

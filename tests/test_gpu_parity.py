@@ -306,3 +306,52 @@ def test_table2_known_answer_counts(golden):
         _, rep = G.solve_stationary(A, f, G.WeightSchedule(omega=d[f"e{k}_omega"]))
         assert rep.iterations == d[f"e{k}_iterations"]
         assert rep.inner_iterations == d[f"e{k}_inner"]
+
+
+@pytest.mark.parametrize("variant", ["plain", "nag"])
+def test_batch_above_64_systems_blocked(variant):
+    """70 systems on 79^2 grids: the blocked sweep runs in launches of at most
+    64 systems (kernel-parameter coefficients).  plain: Jacobi + Leja-ordered
+    Chebyshev weights, systems converge at different sweeps and are skipped
+    afterwards; nag: the same weights with momentum 0.3, most systems
+    diverge at different inner indices.  Systems 0, 63, 64, 69 and a random
+    one equal their own oracle runs: bitwise iterates and counts, or the same
+    DivergenceError inner index."""
+    rng = np.random.default_rng(70)
+    B, n, m = 70, 80, 8
+    probs = [G.AnisotropicProblem(10 ** rng.uniform(-1, 0), rng.uniform(0, np.pi), n)
+             for _ in range(B)]
+    op = G.GpuStencilOperator.from_problems(probs)
+    F = rng.standard_normal((B, op.P))
+    scheds, P = [], []
+    for p in probs:
+        lmax, lmin = G.stencil_symbol_bounds(G.anisotropic_stencil(p), n)
+        s = 2.0 / 3.0 / G.anisotropic_stencil(p)[4]
+        w = G.leja_order(G.chebyshev_weights(s * lmax, s * lmin, m))
+        if variant == "plain":
+            scheds.append(G.WeightSchedule(omega=w))
+            P.append(G.JacobiScale(np.float64(s)))
+        else:
+            scheds.append(G.WeightSchedule(omega=w * s, alpha=np.full(m, 0.3), variant="nag"))
+    res = G.solve_stationary_batched(op, F, scheds, P if variant == "plain" else None,
+                                     tol=1e-2, max_outer=80)
+    if variant == "plain":
+        assert len({r.iterations for _, r in res}) > 1, "systems should stop at different sweeps"
+    for b in sorted({0, 63, 64, 69, int(rng.integers(1, 62))}):
+        A = O.assemble_anisotropic(probs[b].epsilon, probs[b].theta, n)
+        s = scheds[b]
+        u, rep = res[b]
+        try:
+            if variant == "plain":
+                uo, ro = O.solve_stationary(A, F[b], s.omega, scale=O.jacobi_scale(A), tol=1e-2,
+                                            max_outer=80)
+            else:
+                uo, ro = O.solve_stationary(A, F[b], s.omega, s.alpha, variant="nag", tol=1e-2,
+                                            max_outer=80)
+        except O.OracleDivergence as e:
+            assert u is None and isinstance(rep, G.DivergenceError), b
+            assert rep.inner_iteration == e.inner_iteration, b
+            continue
+        assert rep.iterations == ro["iterations"] and rep.inner_iterations == ro["inner_iterations"]
+        assert np.array_equal(u, uo), b
+        _close_trace(rep.trace, ro["trace"])
