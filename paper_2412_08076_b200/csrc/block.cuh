@@ -49,6 +49,7 @@ struct BlockArgs {
     const S* v_in;
     S* u_out;
     S* v_out;
+    S* r_out;           // residual-only launch (T = 1): r = f - A u at the owned points, no update
     const S* f;
     const double* omega;
     const double* alpha;
@@ -168,7 +169,7 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
     // the T steps' weights, loaded once (a global load after every step's
     // barrier would stall all warps on L2 latency together)
     __shared__ double sw[3][8];
-    if (threadIdx.x < T) {
+    if (threadIdx.x < T && !(T == 1 && a.r_out)) {   // (a residual-only launch has no schedule)
         const int k = a.k0 + threadIdx.x;
         const int si = b * a.m + (k % a.m);
         sw[0][threadIdx.x] = a.omega[si];
@@ -284,8 +285,12 @@ block_kernel(const __grid_constant__ BlockArgs<S> a) {
                     nxt[r][col] = live ? x : szero<C>();
                 } else if (live && (NAG ? owned(r, col) : isown(rr, cc))) {
                     const size_t g = base + (size_t)(gx0 + r) * side + (gy0 + col);
-                    a.u_out[g] = to_s<S>(un);
-                    if (HASV) a.v_out[g] = to_s<S>(vn);
+                    if (T == 1 && a.r_out) {
+                        a.r_out[g] = to_s<S>(rs);                        // fns.py:80 residual
+                    } else {
+                        a.u_out[g] = to_s<S>(un);
+                        if (HASV) a.v_out[g] = to_s<S>(vn);
+                    }
                 }
             });
             if (!last) __syncthreads();

@@ -205,6 +205,7 @@ static int do_block(rg_solver* S_, int T, int norm_first_u, cudaStream_t st) {
     a.u_out = (S*)S_->u[S_->cur ^ 1];
     a.v_in = (const S*)S_->v[S_->cur];
     a.v_out = (S*)S_->v[S_->cur ^ 1];
+    a.r_out = nullptr;
     a.f = (const S*)S_->f;
     a.omega = S_->s.omega;
     a.alpha = S_->s.alpha;
@@ -354,6 +355,7 @@ static int sweep_block(const rg_op* A, const rg_sched* s, int k0, int T, bool ja
     a.u_out = (S*)uout;
     a.v_in = (const S*)vin;
     a.v_out = (S*)vout;
+    a.r_out = nullptr;
     a.f = (const S*)f;
     a.omega = s->omega;
     a.alpha = s->alpha;
@@ -1105,6 +1107,40 @@ int rg_dst2(const rg_dst* D, const double* in, double* out, void* stream) {
     return dst_pass(D, 1, DST_PLAIN, out, out, nullptr, st);
 }
 
+// r = f - A u for a CONST9 float64 operator through the blocked kernel's
+// residual-only T = 1 launch (64 x 64 windows staged in shared memory, the
+// stencil as kernel parameters): ~2x the one-point-per-thread step1 kernel.
+static int resid_const9(const rg_op* A, const double* u, const double* f, double* r, cudaStream_t st) {
+    static thread_local BlockArgs<double> a;
+    memset(&a.epi, 0, sizeof a.epi);
+    a.side = A->d.side;
+    a.P = A->P;
+    a.u_in = u;
+    a.v_in = nullptr;
+    a.u_out = nullptr;
+    a.v_out = nullptr;
+    a.r_out = r;
+    a.f = f;
+    a.omega = a.alpha = a.atil = nullptr;
+    a.m = 1;
+    a.k0 = 0;
+    a.norm_first_u = 0;
+    a.norm_every = 0;
+    block_ntiles(A->d.side, 1, &a.nty);
+    const int B = A->d.batch;
+    for (int b0 = 0; b0 < B; b0 += BLK_MAXB) {
+        const int nsys = B - b0 < BLK_MAXB ? B - b0 : BLK_MAXB;
+        a.b0 = b0;
+        for (int j = 0; j < nsys; ++j) {
+            for (int d = 0; d < 9; ++d) a.coef[j][d] = A->hcoef[(size_t)(b0 + j) * 9 + d];
+            a.scale[j] = 0.0;
+        }
+        const cudaError_t err = launch_block<double, V_PLAIN>(a, 1, false, nsys, st);
+        if (err != cudaSuccess) return fail(RG_ECUDA, "residual launch: %s", cudaGetErrorString(err));
+    }
+    return RG_OK;
+}
+
 int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u, const double* f,
                    void* stream) {
     int rc = check_op(A);
@@ -1113,13 +1149,19 @@ int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u
     if (A->d.dtype != RG_F64) return fail(RG_EUNSUPPORTED, "FNS correction is float64 (fns.py:36)");
     if (A->d.side != D->side || A->d.batch != D->batch) return fail(RG_ESIZE, "plan/operator shape mismatch");
     cudaStream_t st = (cudaStream_t)stream;
-    StepReq q;
-    memset(&q, 0, sizeof q);
-    q.u_in = u;
-    q.f = f;
-    q.r_out = D->work;   // r = f - A u  (a separate pass: measured faster than
-    q.m = 1;             // recomputing the stencil inside the row transform's load)
-    if ((rc = step1(A, q, st))) return rc;
+    // r = f - A u (a separate pass: measured faster than recomputing the
+    // stencil inside the row transform's load)
+    if (A->d.kind == RG_CONST9 && !A->hcoef.empty()) {
+        if ((rc = resid_const9(A, u, f, D->work, st))) return rc;
+    } else {
+        StepReq q;
+        memset(&q, 0, sizeof q);
+        q.u_in = u;
+        q.f = f;
+        q.r_out = D->work;
+        q.m = 1;
+        if ((rc = step1(A, q, st))) return rc;
+    }
     if (D->dense) {   // u += S ((S (r S)) * lam) S
         if ((rc = dst_gemm(D, D->work, true, D->S, false, D->work2, GEMM_STORE, nullptr, st))) return rc;
         if ((rc = dst_gemm(D, D->S, false, D->work2, true, D->work, GEMM_LAM, lam, st))) return rc;
