@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$? > gpurun_out/fns.log
-python profiles/fns_time.py >> gpurun_out/fns.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file gpurun_out/fns_launches.csv python profiles/fns_time.py > gpurun_out/ncu_fns.log 2>&1
+echo base > gpurun_out/c1.log; python profiles/cfg1_probe.py 2>&1 | tail -2 >> gpurun_out/c1.log
+for p in 4096 2048 1024 512 256; do echo "1024 threads, points/CTA $p" >> gpurun_out/c1.log; RICHGPU_LIB=paper_2412_08076_b200/librg_cl1024.so RG_CL_POINTS=$p python profiles/cfg1_probe.py 2>&1 | tail -2 >> gpurun_out/c1.log; done
