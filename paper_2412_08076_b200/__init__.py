@@ -20,8 +20,8 @@ from .schedules import (WeightSchedule, chebyshev_semi_weights, chebyshev_weight
                         stencil_symbol_bounds)
 # the reference's top-level names for the rest of the path (richlab/__init__.py:4-31)
 from .fns import SpectralCorrection, dst2, dst2_inv, fns_lite_step, solve_fns
-from .multigrid import (build_hierarchy, prolongation_matrix, restriction_matrix,
-                        v_cycle)
+from .multigrid import (build_hierarchy, prolong, prolongation_matrix, restrict,
+                        restriction_matrix, v_cycle)
 from .fgmres import FgmresConfig, fgmres
 from .spectral import SpectralBounds, estimate_lambda_max, estimate_lambda_min
 

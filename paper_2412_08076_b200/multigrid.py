@@ -40,6 +40,8 @@ class CoarseSolveError(RuntimeError):
 
 
 def _fw1d(n):
+    if n % 2 != 0:   # multigrid.py:26-27
+        raise ValueError(f"grid side {n} must be even to coarsen")
     nc = n // 2
     r = np.repeat(np.arange(nc - 1), 3)
     c = (2 * np.arange(nc - 1)[:, None] + np.arange(3)[None, :]).reshape(-1)
@@ -64,6 +66,40 @@ def prolongation_matrix(n):
     """multigrid.py:45-49."""
     p1 = (2.0 * _fw1d(n).T).tocsr()
     return _canonical(sp.kron(p1, p1, format="csr"))
+
+
+def _transfer(x, n, coarse_side, fn):
+    """Shared body of restrict / prolong: flat vector(s) -> device kernel."""
+    if n % 2 != 0:
+        raise ValueError(f"grid side {n} must be even to coarsen")
+    host = _is_host(x)
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x))
+    cplx = t.is_complex()
+    t = t.to(device=default_device(), dtype=torch.complex128 if cplx else torch.float64)
+    fine_p, coarse_p = (n - 1) ** 2, (n // 2 - 1) ** 2
+    src_p, dst_p = (fine_p, coarse_p) if coarse_side else (coarse_p, fine_p)
+    if t.shape[-1] != src_p:
+        raise ValueError(f"vector length {t.shape[-1]} does not match the n={n} grid")
+    lead = t.shape[:-1]
+    src = t.reshape(-1, src_p).contiguous()
+    dst = torch.zeros((src.shape[0], dst_p), dtype=src.dtype, device=src.device)
+    dt = L.RG_C128 if cplx else L.RG_F64
+    L.check(fn(dt, src.shape[0], n, L.ptr(src), L.ptr(dst), L.stream_ptr()))
+    out = dst.reshape(*lead, dst_p)
+    return out.cpu().numpy() if host else out
+
+
+def restrict(fine, n):
+    """multigrid.py:52-54: full-weighting restriction of a flat (n-1)^2
+    interior vector (or a batch [..., (n-1)^2]) to the n/2 grid, on the
+    device (bitwise R.matvec)."""
+    return _transfer(fine, n, True, L.load().rg_restrict)
+
+
+def prolong(coarse, n):
+    """multigrid.py:57-59: bilinear interpolation of a flat (n/2-1)^2 vector
+    up to the n grid, on the device (bitwise P.matvec)."""
+    return _transfer(coarse, n, False, L.load().rg_prolong_add)
 
 
 def _csr(A):
