@@ -11,15 +11,17 @@ that mirrors the reference API.
 from .errors import (DIVERGENCE_FACTOR, DimensionMismatch, DivergenceError, IterationState,
                      ShannonViolation, SolveReport, UnsupportedOperator, ZeroDiagonalError)
 from .operator import GpuStencilOperator, JacobiScale, as_operator
-from .precond import Preconditioner, TriangularPreconditioner
+from .precond import Preconditioner, TriangularPreconditioner, apply_preconditioner
 from .problems import (AnisotropicProblem, HelmholtzProblem, anisotropic_stencil,
                        helmholtz_stencil)
 from .richardson import (StationarySolver, inner_update, outer_sweep, solve_stationary,
                          solve_stationary_batched)
-from .schedules import (WeightSchedule, chebyshev_semi_weights, chebyshev_weights, leja_order,
+from .schedules import (WeightSchedule, chebyshev_schedule, chebyshev_semi_schedule,
+                        chebyshev_semi_weights, chebyshev_weights, leja_order,
                         stencil_symbol_bounds)
 # the reference's top-level names for the rest of the path (richlab/__init__.py:4-31)
-from .fns import SpectralCorrection, dst2, dst2_inv, fns_lite_step, solve_fns
+from .fns import (SpectralCorrection, dst2, dst2_inv, fns_lite_step, sine_basis_eigenvalues,
+                  sine_mode, solve_fns)
 from .multigrid import (build_hierarchy, prolong, prolongation_matrix, restrict,
                         restriction_matrix, v_cycle)
 from .fgmres import FgmresConfig, fgmres

@@ -23,7 +23,7 @@ import torch
 
 from . import _lib as L
 from .errors import DivergenceError, SolveReport
-from .operator import GpuStencilOperator
+from .operator import GpuStencilOperator, as_operator
 from .richardson import DeviceSchedule, _is_host, _op_for
 
 _PLANS = {}
@@ -77,6 +77,54 @@ def dst2(x):
 def dst2_inv(x):
     """transforms.py:33-35 (the transform is involutory)."""
     return dst2(x)
+
+
+def sine_mode(n, p, q):
+    """transforms.py:38-43: the (p, q) discrete sine mode on the (n-1)^2
+    interior, flattened (x the first axis)."""
+    i = np.arange(1, n)
+    return np.outer(np.sin(p * np.pi * i / n), np.sin(q * np.pi * i / n)).reshape(-1)
+
+
+def sine_basis_eigenvalues(A, n, chunk=256):
+    """fns.py:60-73: diagonal of A in the orthonormal sine basis (its exact
+    eigenvalues when the basis diagonalises A).
+
+    The reference transforms one unit vector per entry on the host.  Here a
+    constant 9-point operator takes the closed form: with v_p the orthonormal
+    DST-I vectors, <v_p, shift_{+-1} v_p> = cos(pi p / n), so entry (p, q) is
+    sum_{a,b} c[a,b] g_a(p) g_b(q), g_0 = 1, g_{+-1} = cos(pi p / n).  Other
+    operators are transformed on the device, `chunk` sine modes per batch
+    (dst2(A dst2(e_k)))."""
+    op = as_operator(A) if not isinstance(A, GpuStencilOperator) else A
+    if op.side != n - 1:
+        raise ValueError("operator and grid size differ")
+    N = n - 1
+    if op.kind == L.RG_CONST9:
+        c = np.asarray(op._host_stencil[0], dtype=np.float64).reshape(3, 3)
+        cp = np.cos(np.pi * np.arange(1, n) / n)
+        g = np.stack([cp, np.ones(N), cp])           # g_a for a = -1, 0, 1
+        lam = np.zeros((N, N))
+        for a in range(3):
+            for b in range(3):
+                lam = lam + c[a, b] * np.outer(g[a], g[b])
+        return lam.reshape(-1)
+    if op.np_dtype != np.float64 or op.nsets != 1:
+        raise ValueError("sine_basis_eigenvalues needs one real float64 operator (fns.py:60-73)")
+    size = N * N
+    lam = np.empty(size)
+    ops = {}
+    for k0 in range(0, size, chunk):
+        k1 = min(size, k0 + chunk)
+        kb = k1 - k0
+        if kb not in ops:
+            ops[kb] = op.broadcast(kb)
+        idx = torch.arange(kb, device="cuda")
+        E = torch.zeros((kb, size), dtype=torch.float64, device="cuda")
+        E[idx, idx + k0] = 1.0
+        AV = ops[kb].matvec(dst2(E))
+        lam[k0:k1] = dst2(AV)[idx, idx + k0].cpu().numpy()
+    return lam
 
 
 class SpectralCorrection:

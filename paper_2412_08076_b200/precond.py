@@ -110,6 +110,14 @@ class Preconditioner:
         return TriangularPreconditioner(as_operator(A), "ssor", relax)
 
 
+def apply_preconditioner(P, r):
+    """precond.py:125-129: B^{-1} r for a built preconditioner (identity for
+    None).  Device tensors stay on the device."""
+    if P is None:
+        return r if isinstance(r, torch.Tensor) else np.asarray(r)
+    return P.apply(r)
+
+
 def tri_spec(P):
     """(kind, relax) when P is a GS / SOR / SSOR map (ours or richlab's), else None."""
     if isinstance(P, TriangularPreconditioner):

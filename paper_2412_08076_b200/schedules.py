@@ -74,6 +74,16 @@ def chebyshev_semi_weights(lambda_max, m, alpha=1.0 / 30.0):
     return chebyshev_weights(lambda_max, alpha * lambda_max, m)
 
 
+def chebyshev_schedule(lambda_max, lambda_min, m):
+    """schedules.py:77-78."""
+    return WeightSchedule(omega=chebyshev_weights(lambda_max, lambda_min, m))
+
+
+def chebyshev_semi_schedule(lambda_max, m, alpha=1.0 / 30.0):
+    """schedules.py:81-82."""
+    return WeightSchedule(omega=chebyshev_semi_weights(lambda_max, m, alpha))
+
+
 def leja_order(omega):
     """Reorder weights so their roots 1/omega form a Leja sequence: start
     from the largest root, then repeatedly take the remaining root that

@@ -92,6 +92,27 @@ def test_fns_solve_counts_inner_iterations():
     assert np.linalg.norm(f - A.dot(u)) <= 1e-10 * np.linalg.norm(f)
 
 
+def test_sine_basis_eigenvalues_closed_form_and_device():
+    """fns.py:60-73: the CONST9 closed form and the device transform path
+    (on the VAR9 form of the same operator) equal the reference's
+    one-vector-at-a-time definition; isotropic case = the closed-form
+    eigenvalues of test_transforms.py:40-52."""
+    n = 12
+    A = O.assemble_anisotropic(0.3, 0.9, n)
+    size = (n - 1) ** 2
+    ref = np.array([O.dst2(A.dot(O.dst2(np.eye(size)[k])))[k] for k in range(size)])
+    lam = G.sine_basis_eigenvalues(A, n)
+    assert np.max(np.abs(lam - ref)) <= 1e-13 * np.max(np.abs(ref))
+    var9 = G.GpuStencilOperator("var9", n - 1, G.GpuStencilOperator.from_sparse(A)._full_planes(),
+                                None, np.float64)
+    lam2 = G.sine_basis_eigenvalues(var9, n, chunk=50)
+    assert np.max(np.abs(lam2 - ref)) <= 1e-13 * np.max(np.abs(ref))
+    iso = G.sine_basis_eigenvalues(O.assemble_anisotropic(1.0, 0.0, n), n).reshape(n - 1, n - 1)
+    cp = np.cos(np.pi * np.arange(1, n) / n)
+    expect = (8.0 - 2.0 * cp[:, None] - 2.0 * cp[None, :] - 4.0 * cp[:, None] * cp[None, :]) / 3.0
+    assert np.max(np.abs(iso - expect)) <= 1e-13 * np.max(expect)
+
+
 # ---------------------------------------------------------- multigrid.py
 def test_vcycle_zero_fixed_point():
     """test_multigrid.py:79-83."""
