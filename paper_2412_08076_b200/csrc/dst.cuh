@@ -5,22 +5,26 @@
 // its odd extension y of length 2M (y_j = x_j, y_{2M-j} = -x_j, y_0 = y_M = 0):
 //   Y_k = -2i sum_j x_j sin(pi j k / M)   =>   DST_k = -Im(Y_k) / 2.
 // The real length-2M FFT is computed as one complex length-M FFT of
-// z_j = y_{2j} + i y_{2j+1} (Stockham radix-4, ping-pong in shared memory,
-// natural order), followed by the even/odd split
+// z_j = y_{2j} + i y_{2j+1}, followed by the even/odd split
 //   Y_k = E_k + e^{-i pi k/M} O_k,  E_k = (Z_k + conj Z_{M-k})/2,
 //                                   O_k = (Z_k - conj Z_{M-k})/(2i).
+// The complex FFT is an in-place Stockham FFT in shared memory: every
+// thread holds 16 values in registers, radix-16 passes (then one radix-2/4/8
+// pass), one load / sync / store per pass; line buffers are XOR-swizzled and
+// padded so every pass and both line orientations are bank-conflict free.
 // Orthonormal scaling sqrt(2/M) per axis (scipy dstn type=1 norm="ortho").
-// Twiddles come from a host-built table tw[k] = (cos(pi k/M), sin(pi k/M)).
+// Twiddles come from a host-built table tw[k] = (cos(pi k/M), sin(pi k/M)),
+// copied to shared memory for M <= DST_SMEM_TW_MAX.
 //
 // Row lines are contiguous; column lines are strided by N and are loaded
 // LPC columns at a time so every row contributes one 32 B+ segment.
 // Not bitwise equal to pocketfft: agreement is ~1e-15 relative (the FNS
-// parity bar is 1e-12, SURVEY.md §8(d) cfg 4).
+// parity bar is 1e-12, SURVEY.md §8(d) cfg 4).  Sizes with M not a power of
+// two take the dense sine-matrix path at the end of this file.
 #pragma once
 #include "common.cuh"
 
 namespace rg {
-
 
 struct DstArgs {
     const double* in;    // [B][N][N]
