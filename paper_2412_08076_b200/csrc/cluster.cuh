@@ -31,6 +31,8 @@ namespace cg = cooperative_groups;
 
 constexpr int CL_NT = 256;
 constexpr int CL_MAXC = 16;     // non-portable cluster size limit
+constexpr int CL_MAXM = 16;     // sweep length of the batched-decision loop
+constexpr int CL_MAXW = 64;     // schedules up to this length are staged in shared memory
 
 template <typename S>
 struct ClusterArgs {
@@ -82,6 +84,19 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
 
     const int fields = NAG ? 3 : 2;    // u (+ y ping-pong) | u ping-pong
     for (int q = tid; q < fields * (R + 2) * W; q += CL_NT) U[q] = szero<C>();
+    // the schedule in shared memory: every cluster barrier invalidates L1
+    // (CCTL.IVALL), so a global weight load after it would cost an L2 round
+    // trip on every inner step's critical path
+    __shared__ double wsm[3][CL_MAXW];
+    const bool wstaged = m <= CL_MAXW;
+    for (int q = tid; q < m && q < CL_MAXW; q += CL_NT) {
+        wsm[0][q] = a.omega[b * m + q];
+        wsm[1][q] = HASV ? a.alpha[b * m + q] : 0.0;
+        wsm[2][q] = NAG ? a.atil[b * m + q] : 0.0;
+    }
+    auto W_ = [&](int i) { return wstaged ? wsm[0][i] : a.omega[b * m + i]; };
+    auto AL_ = [&](int i) { return HASV ? (wstaged ? wsm[1][i] : a.alpha[b * m + i]) : 0.0; };
+    auto AT_ = [&](int i) { return wstaged ? wsm[2][i] : a.atil[b * m + i]; };
     __syncthreads();
 
     C fr[PPT], rr[PPT], vr[PPT];
@@ -202,7 +217,79 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
             status = ST_MAXED;
         }
     };
-    if (!NAG && status == ST_ACTIVE) {
+    if (!NAG && status == ST_ACTIVE && !cf.check_inner && m <= CL_MAXM) {
+        // plain / mom, check = "outer": the decision logic only needs the
+        // sweep-boundary norm for convergence / max_outer, and the per-step
+        // norms for the divergence guard, which it can examine after the
+        // sweep in step order (the first offending inner index is still the
+        // one reported; a diverged solve returns no iterate).  So each inner
+        // step costs one cluster barrier (halo exchange) and a shared-memory
+        // store of the thread's |r|^2; the m per-step norms of a sweep are
+        // reduced together, published with one more barrier and decided in
+        // order.  u ping-pongs (step j reads Ub[j&1], writes Ub[(j+1)&1]);
+        // a boundary stop returns the current iterate.
+        __shared__ double accs[CL_MAXM][CL_NT];            // this thread's |r_j|^2
+        __shared__ double redm[CL_MAXM][CL_NT / 32];
+        __shared__ double partsm[2][CL_MAXM][CL_MAXC];     // by sweep parity
+        C* Ub[2] = {U, U + (R + 2) * W};
+        for (int sweep = 0; status == ST_ACTIVE; ++sweep) {
+            for (int i = 0; i < m; ++i) {                 // steps k .. k+m-1 (i = k % m)
+                const double w = W_(i);
+                const double al = AL_(i);
+                const C* Uo = Ub[k & 1];
+                C* Un = Ub[(k + 1) & 1];
+                C* up_nb = crank > 0 ? cl.map_shared_rank(Un, crank - 1) : nullptr;
+                C* dn_nb = crank < nc - 1 ? cl.map_shared_rank(Un, crank + 1) : nullptr;
+#pragma unroll
+                for (int j = 0; j < PPT; ++j) {                 // (:120-121)
+                    const int pp = tid + j * CL_NT;
+                    if (pp < npts) {
+                        const C p = JAC ? mul(sc, rr[j]) : rr[j];
+                        C vn = (VAR == V_PLAIN) ? rmul(w, p) : add(rmul(al, vr[j]), rmul(w, p));
+                        const C un = stored<S>(add(Uo[pix[j]], vn));
+                        Un[pix[j]] = un;
+                        vr[j] = stored<S>(vn);
+                        // neighbours' halo rows of Un, visible after the barrier;
+                        // they last read them one barrier earlier (ping-pong)
+                        if (pp < s && up_nb) up_nb[(R + 1) * W + pix[j] - W] = un;
+                        if (pp >= npts - s && dn_nb) dn_nb[pix[j] - nrows * W] = un;
+                    }
+                }
+                cl.sync();
+                accs[i][tid] = residual_of(Un);          // r_{k+1}
+                ++k;
+            }
+            // the sweep's m norms: warp sums, CTA partials to every CTA, decide
+            const int lane = tid & 31, wq = tid >> 5;
+            for (int i = 0; i < m; ++i) {
+                double v = accs[i][tid];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+                if (lane == 0) redm[i][wq] = v;
+            }
+            __syncthreads();
+            double (*pm)[CL_MAXC] = partsm[sweep & 1];
+            for (int t = tid; t < m * nc; t += CL_NT) {       // (step, destination CTA)
+                const int i = t / nc, r = t - (t / nc) * nc;
+                double sum = 0.0;
+#pragma unroll
+                for (int q = 0; q < CL_NT / 32; ++q) sum += redm[i][q];
+                *cl.map_shared_rank(&pm[i][crank], r) = sum;
+            }
+            cl.sync();
+            const int j0 = k - m + 1;                         // first inner index of the sweep
+            for (int i = 0; i < m && status == ST_ACTIVE; ++i) {
+                double tot = 0.0;
+                for (int r = 0; r < nc; ++r) tot += pm[i][r];
+                decide(j0 + i, tot);
+            }
+            if (status != ST_ACTIVE) {
+                k = inner;                                    // the decided index
+                Uout = Ub[k & 1];
+            }
+        }
+        cl.sync();                        // last remote writes to partsm complete
+    } else if (!NAG && status == ST_ACTIVE) {
         // plain / mom: ONE cluster barrier per inner step.  The u field is
         // ping-ponged (iteration j reads Ub[j&1], writes Ub[(j+1)&1]), so a
         // neighbour may start its next update while this CTA still copies
@@ -215,8 +302,8 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
         bool have_prev = false;           // partials of r_k available (k >= 1)
         while (true) {
             const int i = k % m;
-            const double w = a.omega[b * m + i];
-            const double al = HASV ? a.alpha[b * m + i] : 0.0;
+            const double w = W_(i);
+            const double al = AL_(i);
             const C* Uo = Ub[k & 1];
             C* Un = Ub[(k + 1) & 1];
             C* up_nb = crank > 0 ? cl.map_shared_rank(Un, crank - 1) : nullptr;
@@ -269,11 +356,11 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
     }
     while (NAG && status == ST_ACTIVE) {
         const int i = k % m;
-        const double w = a.omega[b * m + i];
-        const double al = HASV ? a.alpha[b * m + i] : 0.0;
+        const double w = W_(i);
+        const double al = AL_(i);
         if (NAG) {
             C* Y = Yb[k & 1];
-            const double at = a.atil[b * m + i];
+            const double at = AT_(i);
 #pragma unroll
             for (int j = 0; j < PPT; ++j)
                 if (tid + j * CL_NT < npts) Y[pix[j]] = add(U[pix[j]], rmul(at, vr[j]));   // (:119)
