@@ -231,6 +231,10 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
         __shared__ double accs[CL_MAXM][CL_NT];            // this thread's |r_j|^2
         __shared__ double redm[CL_MAXM][CL_NT / 32];
         __shared__ double partsm[2][CL_MAXM][CL_MAXC];     // by sweep parity
+        __shared__ double tots[CL_MAXM];
+        // tot <= fast_lim  =>  sqrt(tot) / fnorm <= div_thr / 2 (with margin;
+        // an overflowing bound is +inf, still conservative)
+        const double fast_lim = 0.25 * (div_thr * fnorm) * (div_thr * fnorm);
         C* Ub[2] = {U, U + (R + 2) * W};
         for (int sweep = 0; status == ST_ACTIVE; ++sweep) {
             for (int i = 0; i < m; ++i) {                 // steps k .. k+m-1 (i = k % m)
@@ -277,10 +281,27 @@ __global__ void __launch_bounds__(CL_NT, 1) cluster_solve_kernel(ClusterArgs<S> 
                 *cl.map_shared_rank(&pm[i][crank], r) = sum;
             }
             cl.sync();
+            // the m cluster totals in parallel (thread i: pairwise tree over
+            // the nc partials, the same bits in every CTA) ...
+            if (tid < m) {
+                double v[CL_MAXC];
+#pragma unroll
+                for (int r = 0; r < CL_MAXC; ++r) v[r] = r < nc ? pm[tid][r] : 0.0;
+#pragma unroll
+                for (int h = CL_MAXC / 2; h > 0; h >>= 1)
+#pragma unroll
+                    for (int r = 0; r < h; ++r) v[r] = v[r] + v[r + h];
+                tots[tid] = v[0];
+            }
+            __syncthreads();
+            // ... then the decisions in step order.  A non-boundary step whose
+            // total is finite and below a quarter of the squared divergence
+            // threshold can neither raise nor stop: its sqrt / division are
+            // skipped (decide() only runs where it can change the state).
             const int j0 = k - m + 1;                         // first inner index of the sweep
             for (int i = 0; i < m && status == ST_ACTIVE; ++i) {
-                double tot = 0.0;
-                for (int r = 0; r < nc; ++r) tot += pm[i][r];
+                const double tot = tots[i];
+                if (i < m - 1 && tot <= fast_lim && isfinite(tot)) continue;
                 decide(j0 + i, tot);
             }
             if (status != ST_ACTIVE) {
