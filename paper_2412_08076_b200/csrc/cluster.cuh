@@ -444,7 +444,8 @@ inline void cluster_shape(int side, int* nc, int* rows, int* ppt) {
     if ((long long)R * side > 16LL * CL_NT || (c - 1) * R >= side) { *nc = 0; return; }
     *nc = c;
     *rows = R;
-    *ppt = (R * side + CL_NT - 1) / CL_NT <= 4 ? 4 : 16;
+    const int need = (R * side + CL_NT - 1) / CL_NT;   // points per thread
+    *ppt = need <= 1 ? 1 : (need <= 4 ? 4 : 16);
 }
 
 template <typename S>
@@ -481,6 +482,12 @@ cudaError_t launch_cluster(const ClusterArgs<S>& a, int variant, bool jac, int p
                            cudaStream_t st) {
     const size_t smem = cluster_smem_bytes<S>(a.side, a.rows, variant);
 #define RG_CL(V, J, PP) return launch_cluster_k<S, V, J, PP>(a, B, smem, st)
+    if (ppt == 1) {
+        if (variant == V_PLAIN) { if (jac) RG_CL(V_PLAIN, true, 1); RG_CL(V_PLAIN, false, 1); }
+        if (variant == V_MOM) { if (jac) RG_CL(V_MOM, true, 1); RG_CL(V_MOM, false, 1); }
+        if (jac) RG_CL(V_NAG, true, 1);
+        RG_CL(V_NAG, false, 1);
+    }
     if (ppt == 4) {
         if (variant == V_PLAIN) { if (jac) RG_CL(V_PLAIN, true, 4); RG_CL(V_PLAIN, false, 4); }
         if (variant == V_MOM) { if (jac) RG_CL(V_MOM, true, 4); RG_CL(V_MOM, false, 4); }
