@@ -51,6 +51,19 @@ __global__ void __launch_bounds__(NT) psweep_kernel(const __grid_constant__ PsAr
     const size_t nth = (size_t)cl.num_blocks() * blockDim.x;
     const size_t gt = (size_t)cl.block_rank() * blockDim.x + threadIdx.x;
     const size_t base = (size_t)b * P;
+    // the steps' weights in shared memory: every cluster barrier invalidates
+    // L1, so a per-step global weight load would be another L2 round trip
+    constexpr int PS_MAXW = 64;
+    __shared__ double wsm[3][PS_MAXW];
+    const bool wstaged = a.n_steps <= PS_MAXW;
+    for (int t = threadIdx.x; t < a.n_steps && t < PS_MAXW; t += blockDim.x) {
+        const int k = a.k0 + t;
+        const int si = b * a.m + (k % a.m);
+        wsm[0][t] = a.omega[si];
+        wsm[1][t] = HASV ? a.alpha[si] : 0.0;
+        wsm[2][t] = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+    }
+    __syncthreads();
     // y_0: the stencil input of step k0
     for (size_t q = base + gt; q < base + P; q += nth) {
         C x = to_c(a.u[q]);
@@ -77,17 +90,17 @@ __global__ void __launch_bounds__(NT) psweep_kernel(const __grid_constant__ PsAr
             if (a.precond == P_JSCALAR) p = mul(a.scale[b], r);
             else if (a.precond == P_JFIELD) p = mul(a.scale[q], r);
             const int si = b * a.m + (k % a.m);
-            const double w = a.omega[si];
+            const double w = wstaged ? wsm[0][t] : a.omega[si];
             const C ui = to_c(a.u[q]);
             C vn;
             if (VAR == V_PLAIN) vn = rmul(w, p);
-            else vn = add(rmul(a.alpha[si], to_c(a.v[q])), rmul(w, p));
+            else vn = add(rmul(wstaged ? wsm[1][t] : a.alpha[si], to_c(a.v[q])), rmul(w, p));
             const S vs = to_s<S>(vn);
             const S us = to_s<S>(add(ui, vn));
             a.u[q] = us;
             if (HASV) a.v[q] = vs;
             C x = to_c(us);
-            if (NAG) x = add(x, rmul(a.atil[b * a.m + ((k + 1) % a.m)], to_c(vs)));
+            if (NAG) x = add(x, rmul(wstaged ? wsm[2][t] : a.atil[b * a.m + ((k + 1) % a.m)], to_c(vs)));
             nxt[q] = to_s<S>(x);
         }
         cl.sync();
