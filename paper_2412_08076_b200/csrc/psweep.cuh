@@ -71,6 +71,88 @@ __global__ void __launch_bounds__(NT) psweep_kernel(const __grid_constant__ PsAr
         a.y0[q] = to_s<S>(x);
     }
     cl.sync();
+    if (NT == PS_NT && P <= nth) {
+        // one point per thread: u, v, f, the Jacobi scale and the point's
+        // operator row live in registers for all steps; only the stencil
+        // input y crosses threads (L2 ping-pong).  Same arithmetic, in the
+        // same order, as apply_op / the generic loop below.
+        const size_t q = base + gt;
+        const bool mine = gt < P;
+        const int i = (int)(gt / side), j = (int)(gt - (size_t)i * side);
+        const int bc = a.A.shared ? 0 : b;
+        C cf[9], dg = szero<C>();
+#pragma unroll
+        for (int d = 0; d < 9; ++d) cf[d] = szero<C>();
+        C ur = szero<C>(), vr = szero<C>(), fr = szero<C>(), sr = szero<C>();
+        if (mine) {
+            if (KIND == K_CONST9) {
+#pragma unroll
+                for (int d = 0; d < 9; ++d) cf[d] = a.A.stencil[(size_t)bc * 9 + d];
+            } else if (KIND == K_DIAG5) {
+#pragma unroll
+                for (int d = 0; d < 4; ++d) cf[d] = a.A.stencil[(size_t)bc * 4 + d];
+                dg = a.A.diag[(size_t)bc * a.A.P + gt];
+            } else {
+#pragma unroll
+                for (int d = 0; d < 9; ++d) cf[d] = a.A.stencil[((size_t)bc * 9 + d) * a.A.P + gt];
+            }
+            ur = to_c(a.u[q]);
+            if (HASV) vr = to_c(a.v[q]);
+            fr = to_c(a.f[q]);
+            if (a.precond == P_JSCALAR) sr = a.scale[b];
+            else if (a.precond == P_JFIELD) sr = a.scale[q];
+        }
+        for (int t = 0; t < a.n_steps; ++t) {
+            const int k = a.k0 + t;
+            const S* y = ((t & 1) ? a.y1 : a.y0) + base;
+            S* nxt = (t & 1) ? a.y0 : a.y1;
+            if (mine) {
+                auto X = [&](int di, int dj) -> C {
+                    const int ii = i + di, jj = j + dj;
+                    if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
+                    return to_c(y[gt + (ptrdiff_t)di * side + dj]);
+                };
+                C s;
+                if (KIND == K_DIAG5) {                      // apply_op<DIAG5> order
+                    s = mul(cf[0], X(-1, 0));
+                    s = add(s, mul(cf[1], X(0, -1)));
+                    s = add(s, mul(dg, X(0, 0)));
+                    s = add(s, mul(cf[2], X(0, 1)));
+                    s = add(s, mul(cf[3], X(1, 0)));
+                } else {                                    // CSR column order
+                    s = mul(cf[0], X(-1, -1));
+                    s = add(s, mul(cf[1], X(-1, 0)));
+                    s = add(s, mul(cf[2], X(-1, 1)));
+                    s = add(s, mul(cf[3], X(0, -1)));
+                    s = add(s, mul(cf[4], X(0, 0)));
+                    s = add(s, mul(cf[5], X(0, 1)));
+                    s = add(s, mul(cf[6], X(1, -1)));
+                    s = add(s, mul(cf[7], X(1, 0)));
+                    s = add(s, mul(cf[8], X(1, 1)));
+                }
+                const C r = sub(fr, s);
+                const C p = a.precond != P_NONE ? mul(sr, r) : r;   // precond.py:125-129
+                const int si = b * a.m + (k % a.m);
+                const double w = wstaged ? wsm[0][t] : a.omega[si];
+                C vn;
+                if (VAR == V_PLAIN) vn = rmul(w, p);
+                else vn = add(rmul(wstaged ? wsm[1][t] : a.alpha[si], vr), rmul(w, p));
+                const S vs = to_s<S>(vn);
+                const S us = to_s<S>(add(ur, vn));
+                ur = to_c(us);
+                vr = to_c(vs);
+                C x = ur;
+                if (NAG) x = add(x, rmul(wstaged ? wsm[2][t] : a.atil[b * a.m + ((k + 1) % a.m)], vr));
+                nxt[q] = to_s<S>(x);
+            }
+            cl.sync();
+        }
+        if (mine) {
+            a.u[q] = to_s<S>(ur);
+            if (HASV) a.v[q] = to_s<S>(vr);
+        }
+        return;
+    }
     for (int t = 0; t < a.n_steps; ++t) {
         const int k = a.k0 + t;
         const S* cur = (t & 1) ? a.y1 : a.y0;
