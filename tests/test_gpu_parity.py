@@ -355,3 +355,38 @@ def test_batch_above_64_systems_blocked(variant):
         assert rep.iterations == ro["iterations"] and rep.inner_iterations == ro["inner_iterations"]
         assert np.array_equal(u, uo), b
         _close_trace(rep.trace, ro["trace"])
+
+
+@pytest.mark.parametrize("m,check,variant", [(20, "outer", "plain"), (8, "inner", "plain"),
+                                             (20, "outer", "mom"), (12, "inner", "mom")])
+def test_cluster_solver_decision_paths(m, check, variant):
+    """The single-launch cluster solver's two plain/mom loops: the per-sweep
+    batched decision (check="outer", m <= 16) and the per-step lagged one
+    (check="inner" or m > 16), against the oracle: bitwise iterates, equal
+    counts, traces within 1e-12; a divergent schedule raises at the same
+    inner index."""
+    rng = np.random.default_rng(m)
+    A = O.assemble_anisotropic(0.2, 0.6, 48)
+    f = rng.standard_normal(A.shape[0])
+    lam = np.linalg.eigvalsh(A.toarray())
+    w = G.leja_order(G.chebyshev_weights(lam[-1], lam[0], m))
+    al = np.full(m, 0.1) if variant == "mom" else None
+    s = G.WeightSchedule(omega=w, alpha=al, variant=variant) if al is not None else \
+        G.WeightSchedule(omega=w)
+    if variant == "mom":   # heavy ball: constant 1/lambda_max, alpha 0.8
+        w, al = np.full(m, 1.0 / lam[-1]), np.full(m, 0.8)
+        s = G.WeightSchedule(omega=w, alpha=al, variant=variant)
+    u, rep = G.solve_stationary(A, f, s, tol=1e-7, check=check, max_outer=2000)
+    uo, ro = O.solve_stationary(A, f, w, al, variant=variant, tol=1e-7, check=check,
+                                max_outer=2000)
+    assert ro["converged"]
+    assert rep.iterations == ro["iterations"] and rep.inner_iterations == ro["inner_iterations"]
+    assert np.array_equal(u, uo)
+    _close_trace(rep.trace, ro["trace"])
+    # divergence: weights far above 2 / lambda_max
+    sd = G.WeightSchedule(omega=np.full(m, 3.0 / lam[-1]))
+    with pytest.raises(G.DivergenceError) as ei:
+        G.solve_stationary(A, f, sd, tol=1e-7, check=check, max_outer=2000)
+    with pytest.raises(O.OracleDivergence) as eo:
+        O.solve_stationary(A, f, np.full(m, 3.0 / lam[-1]), tol=1e-7, check=check, max_outer=2000)
+    assert ei.value.inner_iteration == eo.value.inner_iteration
