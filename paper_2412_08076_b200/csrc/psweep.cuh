@@ -15,6 +15,7 @@
 // steps at 63^2 take 50 us against 102 us.
 #pragma once
 #include <cooperative_groups.h>
+#include <stdlib.h>
 #include "step.cuh"
 
 namespace rg {
@@ -189,6 +190,185 @@ __global__ void __launch_bounds__(NT) psweep_kernel(const __grid_constant__ PsAr
     }
 }
 
+// ---- row-block variant: the stencil input in distributed shared memory ----
+// For grids with at most 16 x 256 unknowns the L2 round trip of the y
+// ping-pong dominates a psweep step (~2.7 us).  Here CTA c of the cluster
+// owns rows [c R, c R + R) and keeps them, with one halo row above and below
+// and a zero border, in two shared-memory y fields; every step each thread
+// updates its point (u, v, f, the Jacobi scale and the operator row live in
+// registers), writes y_{k+1} into the other field and pushes the CTA's
+// boundary rows straight into the neighbours' halo rows (DSMEM) before the
+// cluster barrier, as the cluster solver does.  Same arithmetic as
+// step1_kernel / psweep_kernel, operation for operation.
+constexpr int CS_NT = 256;
+
+// RG_CSWEEP=0 keeps the L2 ping-pong kernel for comparison
+inline bool csweep_on() {
+    static int v = -1;
+    if (v < 0) {
+        const char* ev = getenv("RG_CSWEEP");
+        v = ev ? atoi(ev) : 1;
+    }
+    return v != 0;
+}
+
+// rows per CTA for a side x side grid on nc <= 16 CTAs (0: does not fit)
+inline int csweep_shape(int side, int* nc) {
+    for (int c = 1; c <= 16; ++c) {
+        const int R = (side + c - 1) / c;
+        if (R * side <= CS_NT && (c - 1) * R < side) { *nc = c; return R; }
+    }
+    *nc = 0;
+    return 0;
+}
+
+template <typename S, int KIND, int VAR>
+__global__ void __launch_bounds__(CS_NT) csweep_kernel(const __grid_constant__ PsArgs<S> a, int R) {
+    typedef CT<S> C;
+    constexpr bool NAG = VAR >= V_NAG;
+    constexpr bool HASV = VAR != V_PLAIN;
+    namespace cgp = cooperative_groups;
+    cgp::cluster_group cl = cgp::this_cluster();
+    const int nc = cl.num_blocks();
+    const int crank = (int)cl.block_rank();
+    const int b = blockIdx.x / nc;
+    const int side = a.A.side, W = side + 2;
+    const size_t base = (size_t)b * a.A.P;
+    const int row0 = crank * R;
+    const int nrows = min(R, side - row0);
+    const int npts = nrows * side;
+    const int tid = threadIdx.x;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C* Yb[2] = {reinterpret_cast<C*>(smem_raw), reinterpret_cast<C*>(smem_raw) + (R + 2) * W};
+    for (int q = tid; q < 2 * (R + 2) * W; q += CS_NT) Yb[0][q] = szero<C>();   // zero border
+
+    constexpr int MAXW = 64;
+    __shared__ double wsm[3][MAXW];
+    const bool wstaged = a.n_steps <= MAXW;
+    for (int t = tid; t < a.n_steps && t < MAXW; t += CS_NT) {
+        const int k = a.k0 + t;
+        const int si = b * a.m + (k % a.m);
+        wsm[0][t] = a.omega[si];
+        wsm[1][t] = HASV ? a.alpha[si] : 0.0;
+        wsm[2][t] = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
+    }
+
+    const bool mine = tid < npts;
+    const int lr = tid / side, col = tid - (tid / side) * side;
+    const int i = row0 + lr;                                  // grid row
+    const size_t g = base + (size_t)i * side + col;
+    const int pix = (lr + 1) * W + col + 1;
+    const int bc = a.A.shared ? 0 : b;
+    C cf[9], dg = szero<C>();
+#pragma unroll
+    for (int d = 0; d < 9; ++d) cf[d] = szero<C>();
+    C ur = szero<C>(), vr = szero<C>(), fr = szero<C>(), sr = szero<C>();
+    if (mine) {
+        const size_t gi = (size_t)i * side + col;
+        if (KIND == K_CONST9) {
+#pragma unroll
+            for (int d = 0; d < 9; ++d) cf[d] = a.A.stencil[(size_t)bc * 9 + d];
+        } else if (KIND == K_DIAG5) {
+#pragma unroll
+            for (int d = 0; d < 4; ++d) cf[d] = a.A.stencil[(size_t)bc * 4 + d];
+            dg = a.A.diag[(size_t)bc * a.A.P + gi];
+        } else {
+#pragma unroll
+            for (int d = 0; d < 9; ++d) cf[d] = a.A.stencil[((size_t)bc * 9 + d) * a.A.P + gi];
+        }
+        ur = to_c(a.u[g]);
+        if (HASV) vr = to_c(a.v[g]);
+        fr = to_c(a.f[g]);
+        if (a.precond == P_JSCALAR) sr = a.scale[b];
+        else if (a.precond == P_JFIELD) sr = a.scale[g];
+    }
+    // push this point's y value into Yn (own field) and, for boundary rows,
+    // into the neighbours' halo rows of Yn
+    auto publish = [&](C* Yn, C x) {
+        Yn[pix] = x;
+        if (lr == 0 && crank > 0) cl.map_shared_rank(Yn, crank - 1)[(R + 1) * W + col + 1] = x;
+        if (lr == nrows - 1 && crank < nc - 1) cl.map_shared_rank(Yn, crank + 1)[col + 1] = x;
+    };
+    __syncthreads();                                          // zero border before any push
+    cl.sync();                                                // every CTA zeroed
+    if (mine) {                                               // y_0 = u (+ at v, :119)
+        C x = ur;
+        if (NAG) x = add(x, rmul(a.atil[b * a.m + (a.k0 % a.m)], vr));
+        publish(Yb[0], to_c(to_s<S>(x)));
+    }
+    cl.sync();
+    for (int t = 0; t < a.n_steps; ++t) {
+        const int k = a.k0 + t;
+        const C* Y = Yb[t & 1];
+        C* Yn = Yb[(t + 1) & 1];
+        if (mine) {
+            const int q = pix;
+            C s;
+            if (KIND == K_DIAG5) {                            // apply_op<DIAG5> order
+                s = mul(cf[0], Y[q - W]);
+                s = add(s, mul(cf[1], Y[q - 1]));
+                s = add(s, mul(dg, Y[q]));
+                s = add(s, mul(cf[2], Y[q + 1]));
+                s = add(s, mul(cf[3], Y[q + W]));
+            } else {                                          // CSR column order
+                s = mul(cf[0], Y[q - W - 1]);
+                s = add(s, mul(cf[1], Y[q - W]));
+                s = add(s, mul(cf[2], Y[q - W + 1]));
+                s = add(s, mul(cf[3], Y[q - 1]));
+                s = add(s, mul(cf[4], Y[q]));
+                s = add(s, mul(cf[5], Y[q + 1]));
+                s = add(s, mul(cf[6], Y[q + W - 1]));
+                s = add(s, mul(cf[7], Y[q + W]));
+                s = add(s, mul(cf[8], Y[q + W + 1]));
+            }
+            const C r = sub(fr, s);
+            const C p = a.precond != P_NONE ? mul(sr, r) : r;   // precond.py:125-129
+            const int si = b * a.m + (k % a.m);
+            const double w = wstaged ? wsm[0][t] : a.omega[si];
+            C vn;
+            if (VAR == V_PLAIN) vn = rmul(w, p);
+            else vn = add(rmul(wstaged ? wsm[1][t] : a.alpha[si], vr), rmul(w, p));
+            const S vs = to_s<S>(vn);
+            const S us = to_s<S>(add(ur, vn));
+            ur = to_c(us);
+            vr = to_c(vs);
+            C x = ur;
+            if (NAG) x = add(x, rmul(wstaged ? wsm[2][t] : a.atil[b * a.m + ((k + 1) % a.m)], vr));
+            publish(Yn, to_c(to_s<S>(x)));
+        }
+        cl.sync();   // y_{k+1} and its halos complete; the neighbours read Y one barrier ago
+    }
+    if (mine) {
+        a.u[g] = to_s<S>(ur);
+        if (HASV) a.v[g] = to_s<S>(vr);
+    }
+    cl.sync();   // no CTA exits while a neighbour may still push into it
+}
+
+template <typename S, int KIND, int VAR>
+cudaError_t launch_csweep_t(const PsArgs<S>& a, int nc, int R, cudaStream_t st) {
+    auto kern = csweep_kernel<S, KIND, VAR>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.B * nc);
+    cfg.blockDim = dim3(CS_NT);
+    cfg.dynamicSmemBytes = 2 * (size_t)(R + 2) * (a.A.side + 2) * sizeof(CT<S>);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a, R);
+}
+
 template <typename S, int KIND, int VAR, int NT>
 cudaError_t launch_psweep_n(const PsArgs<S>& a, cudaStream_t st) {
     auto kern = psweep_kernel<S, KIND, VAR, NT>;
@@ -217,6 +397,9 @@ cudaError_t launch_psweep_n(const PsArgs<S>& a, cudaStream_t st) {
 
 template <typename S, int KIND, int VAR>
 cudaError_t launch_psweep_t(const PsArgs<S>& a, cudaStream_t st) {
+    int nc = 0;
+    const int R = csweep_shape(a.A.side, &nc);
+    if (nc > 0 && csweep_on()) return launch_csweep_t<S, KIND, VAR>(a, nc, R, st);
     return a.A.P <= 16 * PS_NT ? launch_psweep_n<S, KIND, VAR, PS_NT>(a, st)
                                : launch_psweep_n<S, KIND, VAR, PS_NT_BIG>(a, st);
 }
