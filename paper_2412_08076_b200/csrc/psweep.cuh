@@ -212,18 +212,22 @@ inline bool csweep_on() {
     return v != 0;
 }
 
-// rows per CTA for a side x side grid on nc <= 16 CTAs (0: does not fit)
-inline int csweep_shape(int side, int* nc) {
+// rows per CTA for a side x side grid on nc <= 16 CTAs of nt threads (0: does not fit)
+inline int csweep_shape(int side, int nt, int* nc) {
     for (int c = 1; c <= 16; ++c) {
         const int R = (side + c - 1) / c;
-        if (R * side <= CS_NT && (c - 1) * R < side) { *nc = c; return R; }
+        if (R * side <= nt && (c - 1) * R < side) { *nc = c; return R; }
     }
     *nc = 0;
     return 0;
 }
 
-template <typename S, int KIND, int VAR>
-__global__ void __launch_bounds__(CS_NT) csweep_kernel(const __grid_constant__ PsArgs<S> a, int R) {
+// NT = 256: the operator row in registers (<= 16 x 256 unknowns); NT = 1024
+// (<= 16 x 1024, e.g. 127^2): the rows of the CTA's points in shared memory
+// (VAR9: 9 values per point), to stay within 64 registers per thread.
+template <typename S, int KIND, int VAR, int NT>
+__global__ void __launch_bounds__(NT) csweep_kernel(const __grid_constant__ PsArgs<S> a, int R) {
+    constexpr bool CSM = NT > CS_NT;
     typedef CT<S> C;
     constexpr bool NAG = VAR >= V_NAG;
     constexpr bool HASV = VAR != V_PLAIN;
@@ -239,13 +243,15 @@ __global__ void __launch_bounds__(CS_NT) csweep_kernel(const __grid_constant__ P
     const int npts = nrows * side;
     const int tid = threadIdx.x;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    (void)CSM;
     C* Yb[2] = {reinterpret_cast<C*>(smem_raw), reinterpret_cast<C*>(smem_raw) + (R + 2) * W};
-    for (int q = tid; q < 2 * (R + 2) * W; q += CS_NT) Yb[0][q] = szero<C>();   // zero border
+    C* cfs = Yb[0] + 2 * (R + 2) * W;                        // CSM: [9][NT] operator rows
+    for (int q = tid; q < 2 * (R + 2) * W; q += NT) Yb[0][q] = szero<C>();   // zero border
 
     constexpr int MAXW = 64;
     __shared__ double wsm[3][MAXW];
     const bool wstaged = a.n_steps <= MAXW;
-    for (int t = tid; t < a.n_steps && t < MAXW; t += CS_NT) {
+    for (int t = tid; t < a.n_steps && t < MAXW; t += NT) {
         const int k = a.k0 + t;
         const int si = b * a.m + (k % a.m);
         wsm[0][t] = a.omega[si];
@@ -272,6 +278,8 @@ __global__ void __launch_bounds__(CS_NT) csweep_kernel(const __grid_constant__ P
 #pragma unroll
             for (int d = 0; d < 4; ++d) cf[d] = a.A.stencil[(size_t)bc * 4 + d];
             dg = a.A.diag[(size_t)bc * a.A.P + gi];
+        } else if (CSM) {
+            for (int d = 0; d < 9; ++d) cfs[d * NT + tid] = a.A.stencil[((size_t)bc * 9 + d) * a.A.P + gi];
         } else {
 #pragma unroll
             for (int d = 0; d < 9; ++d) cf[d] = a.A.stencil[((size_t)bc * 9 + d) * a.A.P + gi];
@@ -311,15 +319,18 @@ __global__ void __launch_bounds__(CS_NT) csweep_kernel(const __grid_constant__ P
                 s = add(s, mul(cf[2], Y[q + 1]));
                 s = add(s, mul(cf[3], Y[q + W]));
             } else {                                          // CSR column order
-                s = mul(cf[0], Y[q - W - 1]);
-                s = add(s, mul(cf[1], Y[q - W]));
-                s = add(s, mul(cf[2], Y[q - W + 1]));
-                s = add(s, mul(cf[3], Y[q - 1]));
-                s = add(s, mul(cf[4], Y[q]));
-                s = add(s, mul(cf[5], Y[q + 1]));
-                s = add(s, mul(cf[6], Y[q + W - 1]));
-                s = add(s, mul(cf[7], Y[q + W]));
-                s = add(s, mul(cf[8], Y[q + W + 1]));
+                auto cd = [&](int d) -> C {
+                    return (CSM && KIND == K_VAR9) ? cfs[d * NT + tid] : cf[d];
+                };
+                s = mul(cd(0), Y[q - W - 1]);
+                s = add(s, mul(cd(1), Y[q - W]));
+                s = add(s, mul(cd(2), Y[q - W + 1]));
+                s = add(s, mul(cd(3), Y[q - 1]));
+                s = add(s, mul(cd(4), Y[q]));
+                s = add(s, mul(cd(5), Y[q + 1]));
+                s = add(s, mul(cd(6), Y[q + W - 1]));
+                s = add(s, mul(cd(7), Y[q + W]));
+                s = add(s, mul(cd(8), Y[q + W + 1]));
             }
             const C r = sub(fr, s);
             const C p = a.precond != P_NONE ? mul(sr, r) : r;   // precond.py:125-129
@@ -345,19 +356,27 @@ __global__ void __launch_bounds__(CS_NT) csweep_kernel(const __grid_constant__ P
     cl.sync();   // no CTA exits while a neighbour may still push into it
 }
 
-template <typename S, int KIND, int VAR>
+template <typename S, int KIND, int VAR, int NT>
 cudaError_t launch_csweep_t(const PsArgs<S>& a, int nc, int R, cudaStream_t st) {
-    auto kern = csweep_kernel<S, KIND, VAR>;
+    auto kern = csweep_kernel<S, KIND, VAR, NT>;
+    const size_t smem = 2 * (size_t)(R + 2) * (a.A.side + 2) * sizeof(CT<S>) +
+                        (NT > CS_NT && KIND == K_VAR9 ? (size_t)9 * NT * sizeof(CT<S>) : 0);
     static bool attr_set = false;
+    static size_t smem_set = 0;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
+    if (smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.B * nc);
-    cfg.blockDim = dim3(CS_NT);
-    cfg.dynamicSmemBytes = 2 * (size_t)(R + 2) * (a.A.side + 2) * sizeof(CT<S>);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -398,8 +417,10 @@ cudaError_t launch_psweep_n(const PsArgs<S>& a, cudaStream_t st) {
 template <typename S, int KIND, int VAR>
 cudaError_t launch_psweep_t(const PsArgs<S>& a, cudaStream_t st) {
     int nc = 0;
-    const int R = csweep_shape(a.A.side, &nc);
-    if (nc > 0 && csweep_on()) return launch_csweep_t<S, KIND, VAR>(a, nc, R, st);
+    int R = csweep_shape(a.A.side, CS_NT, &nc);
+    if (nc > 0 && csweep_on()) return launch_csweep_t<S, KIND, VAR, CS_NT>(a, nc, R, st);
+    R = csweep_shape(a.A.side, 4 * CS_NT, &nc);
+    if (nc > 0 && csweep_on()) return launch_csweep_t<S, KIND, VAR, 4 * CS_NT>(a, nc, R, st);
     return a.A.P <= 16 * PS_NT ? launch_psweep_n<S, KIND, VAR, PS_NT>(a, st)
                                : launch_psweep_n<S, KIND, VAR, PS_NT_BIG>(a, st);
 }
