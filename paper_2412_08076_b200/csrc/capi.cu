@@ -418,7 +418,7 @@ static int cb9_min_side() {
     static int v = -1;
     if (v < 0) {
         const char* ev = getenv("RG_CB9_MINSIDE");   // tuning override
-        v = ev ? atoi(ev) : 384;
+        v = ev ? atoi(ev) : 200;
     }
     return v;
 }
@@ -852,9 +852,9 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
                          s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
     // complex 5-point Helmholtz smoother (V-cycle fine level): blocked sweep
     const bool cblocked = !blocked && A->cblock_ok && s->precond == RG_PRECOND_NONE && block_T != 1;
-    // (large levels only: on a few CTAs the 8-points-per-thread window is
-    // latency-bound, 48 us per 4-step launch at 31^2 against 4 x 6.4 us for
-    // the one-step kernel; measured break-even between 255^2 and 511^2)
+    // (side >= 200: with 16 x 64 windows, 16 steps at 255^2 take 129 us
+    // against 203 us with one-step launches; at 127^2 the resident cluster
+    // sweep is faster, 46 against 71 us)
     const bool cblocked9 = !blocked && A->var9h && s->precond == RG_PRECOND_NONE &&
                            block_T != 1 && (block_T > 1 || A->d.side >= cb9_min_side());
     std::vector<double> hscale;

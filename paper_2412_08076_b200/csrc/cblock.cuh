@@ -229,8 +229,11 @@ namespace rg {
 // order (-1,-1),(-1,0),(-1,1),(0,-1),(0,0),(0,1),(1,-1),(1,0),(1,1),
 // unfused complex products: bitwise the CSR matvec (apply_op<VAR9>).
 
+// window rows: 16 x 64 windows (4-point threads) measured faster than 32 x 64
+// at 511^2 (376 vs 430 us per 16-step smoothing call) and give 255^2 enough
+// CTAs to take the blocked path
 #ifndef CB9_LR
-#define CB9_LR 32
+#define CB9_LR 16
 #endif
 #ifndef CB9_MINB
 #define CB9_MINB 2
