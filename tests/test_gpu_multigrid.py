@@ -98,6 +98,22 @@ def test_vcycle_vs_oracle_larger_and_batched():
         assert _rel(U[b], O.v_cycle(levels, lu, F[b], sd)) <= 1e-13
 
 
+def test_vcycle_vs_oracle_every_smoother_kind():
+    """n = 512 Helmholtz, depth 6: the blocked Galerkin smoother on 511^2 and
+    255^2, the resident cluster sweeps on 127^2 (operator rows in shared
+    memory), 63^2 and 31^2; equals the oracle's V-cycle."""
+    n = 512
+    A = O.assemble_helmholtz(2 * np.pi * n / 10, n)
+    sched = _sched(n)
+    h = GM.build_hierarchy(A, n, coarsest=16, schedules=sched, batch=1)
+    levels, lu = O.build_hierarchy(A, n, coarsest=16)
+    rng = np.random.default_rng(9)
+    f = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+    u = h.apply(torch.as_tensor(f[None]).cuda()).cpu().numpy()[0]
+    sd = dict(omega=sched.omega, alpha=sched.alpha, alpha_tilde=sched.alpha_tilde, variant="nag")
+    assert _rel(u, O.v_cycle(levels, lu, f, sd)) <= 1e-13
+
+
 def test_fgmres_plain_matches_oracle():
     """Unpreconditioned restarted FGMRES(10) on a real anisotropic system, 188
     Arnoldi steps: the dot products are not BLAS-bitwise, and the restarted
