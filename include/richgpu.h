@@ -185,6 +185,12 @@ int rg_dense_apply(int dtype, int batch, int n, const void* M, int shared,
 int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void* v,
                 long long ldv, const void* h, const void* vn, long long ldvn, void* hn,
                 double* wnorm2, void* stream);
+/* One whole modified Gram-Schmidt orthogonalisation of w against
+ * v_0 .. v_k (fgmres.py:76-78), k + 2 rg_mgs_step launches from one call:
+ * v_i = V + i * n elements (system stride ldv), H is [k + 1][batch]
+ * (H[i][b] = h_{i,k} of system b), wnorm2[b] = ||w||^2 afterwards. */
+int rg_mgs_arnoldi(int dtype, int batch, int n, void* w, long long ldw, const void* V,
+                   long long ldv, int k, void* H, double* wnorm2, void* stream);
 
 /* ---- Gauss-Seidel / SOR / SSOR preconditioners (precond.py:79-118) --------
  * z = B^{-1} r for every system of a CONST9 real operator:

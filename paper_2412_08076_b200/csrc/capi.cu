@@ -1249,6 +1249,22 @@ int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void*
     return RG_OK;
 }
 
+int rg_mgs_arnoldi(int dtype, int batch, int n, void* w, long long ldw, const void* V, long long ldv,
+                   int k, void* H, double* wnorm2, void* stream) {
+    if (!w || !V || !H || !wnorm2) return fail(RG_ENULL, "null argument");
+    if (k < 0) return fail(RG_EINVAL, "k must be >= 0");
+    const size_t el = dtype == RG_C128 ? sizeof(double2) : sizeof(double);
+    auto vi = [&](int i) { return (const void*)((const char*)V + (size_t)i * n * el); };
+    auto hi = [&](int i) { return (void*)((char*)H + (size_t)i * batch * el); };
+    // step i applies the projection on v_{i-1} and takes <v_i, w> (:76-78)
+    for (int i = 0; i <= k; ++i) {
+        const int rc = rg_mgs_step(dtype, batch, n, w, ldw, i ? vi(i - 1) : nullptr, ldv,
+                                   i ? hi(i - 1) : nullptr, vi(i), ldv, hi(i), nullptr, stream);
+        if (rc) return rc;
+    }
+    return rg_mgs_step(dtype, batch, n, w, ldw, vi(k), ldv, hi(k), nullptr, 0, nullptr, wnorm2, stream);
+}
+
 int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double tol,
                      int max_outer, int check, int block_T) {
     if (!out) return fail(RG_ENULL, "null out");

@@ -130,14 +130,8 @@ def fgmres_batched(A, F, precond_apply=None, cfg: FgmresConfig = None, U0=None):
                 n2 = torch.empty(B, dtype=torch.float64, device=op.device)
                 ld = (mr + 1) * n
                 code = L.RG_C128 if op.torch_dtype == torch.complex128 else L.RG_F64
-                for i in range(k + 1):
-                    L.check(op._lib.rg_mgs_step(
-                        code, B, n, L.ptr(w), n,
-                        L.ptr(V[:, i - 1]) if i else None, ld, L.ptr(hbuf[i - 1]) if i else None,
-                        L.ptr(V[:, i]), ld, L.ptr(hbuf[i]), None, L.stream_ptr()))
-                L.check(op._lib.rg_mgs_step(code, B, n, L.ptr(w), n, L.ptr(V[:, k]), ld,
-                                            L.ptr(hbuf[k]), None, 0, None, L.ptr(n2),
-                                            L.stream_ptr()))
+                L.check(op._lib.rg_mgs_arnoldi(code, B, n, L.ptr(w), n, L.ptr(V), ld, k,
+                                               L.ptr(hbuf), L.ptr(n2), L.stream_ptr()))
                 hk1 = torch.sqrt(n2)
                 H = hbuf.t()                                  # [G, k+1]
             else:
