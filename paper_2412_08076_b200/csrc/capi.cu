@@ -868,7 +868,14 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     const int T = block_T == 0 ? 5 : block_T;
     int k = i0;
     int left = n_steps;
-    const int TC = block_T == 0 ? 4 : (block_T < 4 ? block_T : 4);
+    // automatic depth of the complex blocked sweeps: 4 for the 32-row 5-point
+    // windows, 3 for the 16-row Galerkin windows (511^2: 305 us per 16-step
+    // call at T=3 against 373 at T=4, 304 at T=2); RG_CB_T / RG_CB9_T override
+    int TC = block_T == 0 ? (cblocked9 ? 3 : 4) : (block_T < 4 ? block_T : 4);
+    if (block_T == 0) {
+        if (const char* ev = getenv(cblocked9 ? "RG_CB9_T" : "RG_CB_T"))
+            TC = atoi(ev) < 1 ? 1 : (atoi(ev) > 4 ? 4 : atoi(ev));
+    }
     // small grids (coarse V-cycle levels): every step in one cooperative launch
     const size_t total = (size_t)A->d.batch * A->P;
     // (one point per thread: a 16-CTA cluster of 1024-thread CTAs covers
