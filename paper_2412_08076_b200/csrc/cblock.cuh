@@ -19,7 +19,10 @@ namespace rg {
 #ifndef CB_LR_ROWS   // window rows of the 5-point smoother (16 measured 724 vs 568 us at 1023^2)
 #define CB_LR_ROWS 32
 #endif
-constexpr int CB_LR = CB_LR_ROWS, CB_LC = 64, CB_NW = 8;
+#ifndef CB_WARPS   // warps per CTA (16 with 1 CTA/SM measured 634 vs 565 us at 1023^2)
+#define CB_WARPS 8
+#endif
+constexpr int CB_LR = CB_LR_ROWS, CB_LC = 64, CB_NW = CB_WARPS;
 #ifndef CB_DIAG_REGS
 #define CB_DIAG_REGS 1
 #endif
