@@ -22,12 +22,18 @@ namespace rg {
 #ifndef CB_WARPS   // warps per CTA (16 with 1 CTA/SM measured 634 vs 565 us at 1023^2)
 #define CB_WARPS 8
 #endif
-constexpr int CB_LR = CB_LR_ROWS, CB_LC = 64, CB_NW = CB_WARPS;
+// 32-column windows, 3 CTAs/SM (4 points per thread, 80 registers): 538 us
+// per 16-step call at 1023^2 against 564 us for 32 x 64 at 2 CTAs/SM
+#ifndef CB_COLS
+#define CB_COLS 32
+#endif
+constexpr int CB_LR = CB_LR_ROWS, CB_LC = CB_COLS, CB_NW = CB_WARPS;
+constexpr int CB9_LC = 64;   // the Galerkin-level windows keep 64 columns
 #ifndef CB_DIAG_REGS
 #define CB_DIAG_REGS 1
 #endif
 #ifndef CB_MINB
-#define CB_MINB 2
+#define CB_MINB 3
 #endif
 
 struct CBlockArgs {
@@ -245,7 +251,7 @@ namespace rg {
 #define CB9_MINB 2
 #endif
 __host__ __device__ inline int cblock9_ntiles(int side, int T, int* nty) {
-    const int TX = CB9_LR - 2 * T, TY = CB_LC - 2 * T;
+    const int TX = CB9_LR - 2 * T, TY = CB9_LC - 2 * T;
     const int ny = (side + TY - 1) / TY;
     if (nty) *nty = ny;
     return ((side + TX - 1) / TX) * ny;
@@ -272,7 +278,7 @@ struct CBlock9Args {
 template <int VAR, int T>
 __global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __grid_constant__ CBlock9Args a) {
     typedef double2 C;
-    constexpr int LR = CB9_LR, LC = CB_LC;
+    constexpr int LR = CB9_LR, LC = CB9_LC;
     constexpr int RPW = LR / CB_NW, CPT = LC / 32;
     constexpr int TX = LR - 2 * T, TY = LC - 2 * T;
     constexpr bool NAG = VAR >= V_NAG;
@@ -406,7 +412,7 @@ __global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __g
 template <int VAR, int T>
 cudaError_t launch_cblock9_t(const CBlock9Args& a0, int batch, cudaStream_t st) {
     auto kern = cblock9_kernel<VAR, T>;
-    const size_t smem = 3 * (size_t)CB9_LR * CB_LC * sizeof(double2);
+    const size_t smem = 3 * (size_t)CB9_LR * CB9_LC * sizeof(double2);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
