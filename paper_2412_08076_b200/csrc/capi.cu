@@ -67,12 +67,8 @@ struct rg_op {
     bool var9h = false;
     double2 hc9[9];
     unsigned char* mask = nullptr;  // device [P] (owned)
-    // small-grid persistent sweep workspace (y ping-pong + grid barrier),
-    // allocated on first use outside stream capture
-    mutable void* ps_ws = nullptr;
     ~rg_op() {
         if (mask) cudaFree(mask);
-        if (ps_ws) cudaFree(ps_ws);
     }
 };
 
@@ -399,18 +395,6 @@ static int chunk_len(int n, int T, int i) {
         start += len;
     }
     return 1;
-}
-
-// largest grid (unknowns per system) swept by the single-launch cluster
-// kernel (psweep.cuh); RG_PS_MAX overrides for tuning
-static size_t ps_max_unknowns() {
-    static long v = -1;
-    if (v < 0) {
-        const char* ev = getenv("RG_PS_MAX");
-        v = ev ? atol(ev) : 16 * PS_NT_BIG;
-        if (v > 16 * PS_NT_BIG) v = 16 * PS_NT_BIG;
-    }
-    return (size_t)v;
 }
 
 // smallest side that takes the blocked 9-point complex sweep automatically
@@ -876,28 +860,14 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
         if (const char* ev = getenv(cblocked9 ? "RG_CB9_T" : "RG_CB_T"))
             TC = atoi(ev) < 1 ? 1 : (atoi(ev) > 4 ? 4 : atoi(ev));
     }
-    // small grids (coarse V-cycle levels): every step in one cooperative launch
-    const size_t total = (size_t)A->d.batch * A->P;
-    // (one point per thread: a 16-CTA cluster of 1024-thread CTAs covers
-    // 16384 unknowns; with 256-thread CTAs and 4 points per thread, 127^2
-    // measured slower than 16 one-step launches: 129 vs 102 us)
-    bool small = !blocked && !cblocked && !cblocked9 && block_T == 0 && n_steps >= 2 &&
-                 (A->d.dtype == RG_F64 || A->d.dtype == RG_C128) && A->P <= ps_max_unknowns();
-    if (small && !A->ps_ws) {
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        cudaStreamIsCapturing(st, &cs);
-        const size_t el = A->d.dtype == RG_C128 ? 16 : 8;
-        if (cs != cudaStreamCaptureStatusNone ||
-            cudaMalloc(&A->ps_ws, 2 * total * el + 256) != cudaSuccess) {
-            small = false;
-            A->ps_ws = nullptr;
-            cudaGetLastError();
-        }
-    }
+    // small grids (coarse V-cycle levels): every step in one cluster launch
+    // with the stencil input resident in distributed shared memory
+    // (psweep.cuh; up to 16 x 1024 unknowns per system)
+    int cs_nc = 0;
+    csweep_shape(A->d.side, CS_NT_BIG, &cs_nc);
+    const bool small = !blocked && !cblocked && !cblocked9 && block_T == 0 && n_steps >= 2 &&
+                       (A->d.dtype == RG_F64 || A->d.dtype == RG_C128) && cs_nc > 0;
     if (small) {
-        const size_t el = A->d.dtype == RG_C128 ? 16 : 8;
-        char* y0 = (char*)A->ps_ws + 256;
-        char* y1 = y0 + total * el;
         cudaError_t err;
         if (A->d.dtype == RG_F64) {
             PsArgs<double> pa;
@@ -905,8 +875,6 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
             pa.u = (double*)u[0];
             pa.v = (double*)v[0];
             pa.f = (const double*)f;
-            pa.y0 = (double*)y0;
-            pa.y1 = (double*)y1;
             pa.omega = s->omega;
             pa.alpha = s->alpha;
             pa.atil = s->alpha_tilde;
@@ -923,8 +891,6 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
             pa.u = (double2*)u[0];
             pa.v = (double2*)v[0];
             pa.f = (const double2*)f;
-            pa.y0 = (double2*)y0;
-            pa.y1 = (double2*)y1;
             pa.omega = s->omega;
             pa.alpha = s->alpha;
             pa.atil = s->alpha_tilde;

@@ -1,18 +1,14 @@
 // psweep.cuh — free-running sweeps of small grids in ONE launch
 // (multigrid.py:126-138 `_smooth` on the coarse V-cycle levels, and any
-// other small rg_sweep).
+// other small rg_sweep of up to 16 x 1024 unknowns per system).
 //
 // On small grids a one-step launch is latency-bound (6.4 us per step at
-// 31^2 .. 127^2 in the cfg5 V-cycle).  Here one
-// thread-block cluster per system (up to 16 CTAs) runs all the steps, with
-// a cluster barrier between steps (a grid-wide software barrier measured
-// ~4 us per step; cluster barriers are hardware): the stencil input y (u,
-// or the NAG look-ahead u + at v) ping-pongs through two L2-resident
-// buffers, u and v are updated in place (pointwise), f and the
-// coefficients stay in L2.  The arithmetic is step1_kernel's, operation for
-// operation (bitwise).  One point per thread: 256-thread CTAs up to 4096
-// unknowns per system, 1024-thread CTAs up to 16384 (127^2); 16 smoothing
-// steps at 63^2 take 50 us against 102 us.
+// 31^2 .. 127^2 in the cfg5 V-cycle).  Here one thread-block cluster per
+// system (up to 16 CTAs) runs all the steps with the stencil input resident
+// in distributed shared memory (csweep_kernel below).  An earlier variant
+// ping-ponged y through L2 with u and v updated in global memory; every
+// cluster barrier invalidates L1, so each of its steps paid two L2 round
+// trips (~2.7 us per step at 63^2 against ~1.3 us here).
 #pragma once
 #include <cooperative_groups.h>
 #include <stdlib.h>
@@ -20,17 +16,12 @@
 
 namespace rg {
 
-constexpr int PS_NT = 256;        // threads per CTA up to 16 * 256 unknowns
-constexpr int PS_NT_BIG = 1024;   // up to 16 * 1024 (127^2): still one point per thread
-
 template <typename S>
 struct PsArgs {
     OpView<S> A;
     S* u;
     S* v;              // null for plain
     const S* f;
-    S* y0;
-    S* y1;
     const double* omega;
     const double* alpha;
     const double* atil;
@@ -38,157 +29,6 @@ struct PsArgs {
     int precond;
     int m, k0, n_steps, B;
 };
-
-template <typename S, int KIND, int VAR, int NT>
-__global__ void __launch_bounds__(NT) psweep_kernel(const __grid_constant__ PsArgs<S> a) {
-    typedef CT<S> C;
-    constexpr bool NAG = VAR >= V_NAG;
-    constexpr bool HASV = VAR != V_PLAIN;
-    namespace cgp = cooperative_groups;
-    cgp::cluster_group cl = cgp::this_cluster();
-    const int side = a.A.side;
-    const size_t P = a.A.P;
-    const int b = blockIdx.x / cl.num_blocks();             // one cluster per system
-    const size_t nth = (size_t)cl.num_blocks() * blockDim.x;
-    const size_t gt = (size_t)cl.block_rank() * blockDim.x + threadIdx.x;
-    const size_t base = (size_t)b * P;
-    // the steps' weights in shared memory: every cluster barrier invalidates
-    // L1, so a per-step global weight load would be another L2 round trip
-    constexpr int PS_MAXW = 64;
-    __shared__ double wsm[3][PS_MAXW];
-    const bool wstaged = a.n_steps <= PS_MAXW;
-    for (int t = threadIdx.x; t < a.n_steps && t < PS_MAXW; t += blockDim.x) {
-        const int k = a.k0 + t;
-        const int si = b * a.m + (k % a.m);
-        wsm[0][t] = a.omega[si];
-        wsm[1][t] = HASV ? a.alpha[si] : 0.0;
-        wsm[2][t] = NAG ? a.atil[b * a.m + ((k + 1) % a.m)] : 0.0;
-    }
-    __syncthreads();
-    // y_0: the stencil input of step k0
-    for (size_t q = base + gt; q < base + P; q += nth) {
-        C x = to_c(a.u[q]);
-        if (NAG) x = add(x, rmul(a.atil[b * a.m + (a.k0 % a.m)], to_c(a.v[q])));
-        a.y0[q] = to_s<S>(x);
-    }
-    cl.sync();
-    if (NT == PS_NT && P <= nth) {
-        // one point per thread: u, v, f, the Jacobi scale and the point's
-        // operator row live in registers for all steps; only the stencil
-        // input y crosses threads (L2 ping-pong).  Same arithmetic, in the
-        // same order, as apply_op / the generic loop below.
-        const size_t q = base + gt;
-        const bool mine = gt < P;
-        const int i = (int)(gt / side), j = (int)(gt - (size_t)i * side);
-        const int bc = a.A.shared ? 0 : b;
-        C cf[9], dg = szero<C>();
-#pragma unroll
-        for (int d = 0; d < 9; ++d) cf[d] = szero<C>();
-        C ur = szero<C>(), vr = szero<C>(), fr = szero<C>(), sr = szero<C>();
-        if (mine) {
-            if (KIND == K_CONST9) {
-#pragma unroll
-                for (int d = 0; d < 9; ++d) cf[d] = a.A.stencil[(size_t)bc * 9 + d];
-            } else if (KIND == K_DIAG5) {
-#pragma unroll
-                for (int d = 0; d < 4; ++d) cf[d] = a.A.stencil[(size_t)bc * 4 + d];
-                dg = a.A.diag[(size_t)bc * a.A.P + gt];
-            } else {
-#pragma unroll
-                for (int d = 0; d < 9; ++d) cf[d] = a.A.stencil[((size_t)bc * 9 + d) * a.A.P + gt];
-            }
-            ur = to_c(a.u[q]);
-            if (HASV) vr = to_c(a.v[q]);
-            fr = to_c(a.f[q]);
-            if (a.precond == P_JSCALAR) sr = a.scale[b];
-            else if (a.precond == P_JFIELD) sr = a.scale[q];
-        }
-        for (int t = 0; t < a.n_steps; ++t) {
-            const int k = a.k0 + t;
-            const S* y = ((t & 1) ? a.y1 : a.y0) + base;
-            S* nxt = (t & 1) ? a.y0 : a.y1;
-            if (mine) {
-                auto X = [&](int di, int dj) -> C {
-                    const int ii = i + di, jj = j + dj;
-                    if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
-                    return to_c(y[gt + (ptrdiff_t)di * side + dj]);
-                };
-                C s;
-                if (KIND == K_DIAG5) {                      // apply_op<DIAG5> order
-                    s = mul(cf[0], X(-1, 0));
-                    s = add(s, mul(cf[1], X(0, -1)));
-                    s = add(s, mul(dg, X(0, 0)));
-                    s = add(s, mul(cf[2], X(0, 1)));
-                    s = add(s, mul(cf[3], X(1, 0)));
-                } else {                                    // CSR column order
-                    s = mul(cf[0], X(-1, -1));
-                    s = add(s, mul(cf[1], X(-1, 0)));
-                    s = add(s, mul(cf[2], X(-1, 1)));
-                    s = add(s, mul(cf[3], X(0, -1)));
-                    s = add(s, mul(cf[4], X(0, 0)));
-                    s = add(s, mul(cf[5], X(0, 1)));
-                    s = add(s, mul(cf[6], X(1, -1)));
-                    s = add(s, mul(cf[7], X(1, 0)));
-                    s = add(s, mul(cf[8], X(1, 1)));
-                }
-                const C r = sub(fr, s);
-                const C p = a.precond != P_NONE ? mul(sr, r) : r;   // precond.py:125-129
-                const int si = b * a.m + (k % a.m);
-                const double w = wstaged ? wsm[0][t] : a.omega[si];
-                C vn;
-                if (VAR == V_PLAIN) vn = rmul(w, p);
-                else vn = add(rmul(wstaged ? wsm[1][t] : a.alpha[si], vr), rmul(w, p));
-                const S vs = to_s<S>(vn);
-                const S us = to_s<S>(add(ur, vn));
-                ur = to_c(us);
-                vr = to_c(vs);
-                C x = ur;
-                if (NAG) x = add(x, rmul(wstaged ? wsm[2][t] : a.atil[b * a.m + ((k + 1) % a.m)], vr));
-                nxt[q] = to_s<S>(x);
-            }
-            cl.sync();
-        }
-        if (mine) {
-            a.u[q] = to_s<S>(ur);
-            if (HASV) a.v[q] = to_s<S>(vr);
-        }
-        return;
-    }
-    for (int t = 0; t < a.n_steps; ++t) {
-        const int k = a.k0 + t;
-        const S* cur = (t & 1) ? a.y1 : a.y0;
-        S* nxt = (t & 1) ? a.y0 : a.y1;
-        for (size_t q = base + gt; q < base + P; q += nth) {
-            const size_t idx = q - base;
-            const int i = (int)(idx / side), j = (int)(idx - (size_t)i * side);
-            const S* y = cur + (size_t)b * P;
-            auto X = [&](int di, int dj) -> C {
-                const int ii = i + di, jj = j + dj;
-                if (ii < 0 || ii >= side || jj < 0 || jj >= side) return szero<C>();
-                return to_c(y[idx + (ptrdiff_t)di * side + dj]);
-            };
-            const C s = apply_op<S, KIND>(a.A, b, idx, X);
-            const C r = sub(to_c(a.f[q]), s);
-            C p = r;                                           // precond.py:125-129
-            if (a.precond == P_JSCALAR) p = mul(a.scale[b], r);
-            else if (a.precond == P_JFIELD) p = mul(a.scale[q], r);
-            const int si = b * a.m + (k % a.m);
-            const double w = wstaged ? wsm[0][t] : a.omega[si];
-            const C ui = to_c(a.u[q]);
-            C vn;
-            if (VAR == V_PLAIN) vn = rmul(w, p);
-            else vn = add(rmul(wstaged ? wsm[1][t] : a.alpha[si], to_c(a.v[q])), rmul(w, p));
-            const S vs = to_s<S>(vn);
-            const S us = to_s<S>(add(ui, vn));
-            a.u[q] = us;
-            if (HASV) a.v[q] = vs;
-            C x = to_c(us);
-            if (NAG) x = add(x, rmul(wstaged ? wsm[2][t] : a.atil[b * a.m + ((k + 1) % a.m)], to_c(vs)));
-            nxt[q] = to_s<S>(x);
-        }
-        cl.sync();
-    }
-}
 
 // ---- row-block variant: the stencil input in distributed shared memory ----
 // For grids with at most 16 x 256 unknowns the L2 round trip of the y
@@ -200,17 +40,8 @@ __global__ void __launch_bounds__(NT) psweep_kernel(const __grid_constant__ PsAr
 // boundary rows straight into the neighbours' halo rows (DSMEM) before the
 // cluster barrier, as the cluster solver does.  Same arithmetic as
 // step1_kernel / psweep_kernel, operation for operation.
-constexpr int CS_NT = 256;
-
-// RG_CSWEEP=0 keeps the L2 ping-pong kernel for comparison
-inline bool csweep_on() {
-    static int v = -1;
-    if (v < 0) {
-        const char* ev = getenv("RG_CSWEEP");
-        v = ev ? atoi(ev) : 1;
-    }
-    return v != 0;
-}
+constexpr int CS_NT = 256;        // operator row in registers (<= 16 x 256 unknowns)
+constexpr int CS_NT_BIG = 1024;   // operator rows in shared memory (<= 16 x 1024)
 
 // rows per CTA for a side x side grid on nc <= 16 CTAs of nt threads (0: does not fit)
 inline int csweep_shape(int side, int nt, int* nc) {
@@ -388,41 +219,14 @@ cudaError_t launch_csweep_t(const PsArgs<S>& a, int nc, int R, cudaStream_t st) 
     return cudaLaunchKernelEx(&cfg, kern, a, R);
 }
 
-template <typename S, int KIND, int VAR, int NT>
-cudaError_t launch_psweep_n(const PsArgs<S>& a, cudaStream_t st) {
-    auto kern = psweep_kernel<S, KIND, VAR, NT>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
-    int cs = (int)((a.A.P + NT - 1) / NT);
-    cs = cs < 1 ? 1 : (cs > 16 ? 16 : cs);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(a.B * cs);
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cs;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, a);
-}
-
 template <typename S, int KIND, int VAR>
 cudaError_t launch_psweep_t(const PsArgs<S>& a, cudaStream_t st) {
     int nc = 0;
     int R = csweep_shape(a.A.side, CS_NT, &nc);
-    if (nc > 0 && csweep_on()) return launch_csweep_t<S, KIND, VAR, CS_NT>(a, nc, R, st);
-    R = csweep_shape(a.A.side, 4 * CS_NT, &nc);
-    if (nc > 0 && csweep_on()) return launch_csweep_t<S, KIND, VAR, 4 * CS_NT>(a, nc, R, st);
-    return a.A.P <= 16 * PS_NT ? launch_psweep_n<S, KIND, VAR, PS_NT>(a, st)
-                               : launch_psweep_n<S, KIND, VAR, PS_NT_BIG>(a, st);
+    if (nc > 0) return launch_csweep_t<S, KIND, VAR, CS_NT>(a, nc, R, st);
+    R = csweep_shape(a.A.side, CS_NT_BIG, &nc);
+    if (nc > 0) return launch_csweep_t<S, KIND, VAR, CS_NT_BIG>(a, nc, R, st);
+    return cudaErrorInvalidValue;   // (the caller checks csweep_shape first)
 }
 
 template <typename S, int KIND>
