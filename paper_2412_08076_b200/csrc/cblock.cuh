@@ -28,7 +28,10 @@ namespace rg {
 #define CB_COLS 32
 #endif
 constexpr int CB_LR = CB_LR_ROWS, CB_LC = CB_COLS, CB_NW = CB_WARPS;
-constexpr int CB9_LC = 64;   // the Galerkin-level windows keep 64 columns
+#ifndef CB9_COLS
+#define CB9_COLS 64   // Galerkin-level windows: 64 columns (16 x 32 at 3 CTAs/SM: 346 vs 303 us at 511^2)
+#endif
+constexpr int CB9_LC = CB9_COLS;
 #ifndef CB_DIAG_REGS
 #define CB_DIAG_REGS 1
 #endif
