@@ -35,6 +35,10 @@ enum { TRI_SOR = 1, TRI_SSOR = 2, TRI_SOR_T = 3, TRI_SSOR_T = 4 };
 // with the lower coefficients, and (D + wU)^{-T} the forward sweep with the
 // upper ones.
 constexpr int TRI_PF = 8;
+// rows per pass (threads per CTA); a grid taller than this runs in passes
+#ifndef RG_TRI_NT_MAX
+#define RG_TRI_NT_MAX 1024
+#endif
 
 template <typename S>
 struct TriArgs {
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(1024, 1) tri_kernel(const TriArgs<S> a) {
 template <typename S, int MODE>
 cudaError_t launch_tri_m(const TriArgs<S>& a, int batch, cudaStream_t st) {
     int nt = (a.side + 31) / 32 * 32;
-    if (nt > 1024) nt = 1024;
+    if (nt > RG_TRI_NT_MAX) nt = RG_TRI_NT_MAX;
     const size_t smem = (2 * (size_t)nt * TRI_WS + a.side) * sizeof(double);
     auto k = tri_kernel<S, MODE>;
     {
