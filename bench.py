@@ -16,6 +16,14 @@ One step = one outer sweep (32 inner updates) over all systems of a GPU.
   roofline  dominant kernel (temporally blocked sweep): algorithmic bytes per
             launch (24 B per point-update) / CUDA-event time
   time_to_tol  wall time of that API solve (all 8 systems to ||r||/||f|| < 1e-6)
+  cpu_time_to_tol  the CPU oracle's time for the same batch to 1e-6, extrapolated
+            from its measured per-core rate x the actual inner iterations
+  e2e_dropin  cfg3 through the reference signature solve_stationary(A_csr,
+            f_numpy, ...) per system (what a migrating richlab user calls)
+  configs   one line per other BASELINE config (cfg1, cfg2 f64/f32, cfg4, cfg5)
+            and the north-star NAG(16) sweep at 8 x 1023^2: value, roofline,
+            e2e, cpu_baseline and an in-run oracle parity check each
+            (bench_configs.py); rank 0 at N=1 only
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
@@ -114,21 +122,23 @@ def _cpu_worker_init(eps, theta, n, seed_f, w):
     A = O.assemble_anisotropic(eps, theta, n)
     f = np.random.default_rng(seed_f).standard_normal(A.shape[0])
     u = np.zeros(A.shape[0])
-    _W = dict(A=A, f=f, u=u, r=f - A.dot(u), scale=O.jacobi_scale(A), w=w, i=0)
+    _W = dict(A=A, f=f, u=u, v=np.zeros_like(u), r=f - A.dot(u), scale=O.jacobi_scale(A), w=w,
+              i=0)
 
 
 def _cpu_worker_steps(k):
     """k inner steps of Jacobi Richardson on this worker's system (the
-    oracle's restatement of richardson.py:111-125, same SciPy/NumPy calls)."""
+    oracle's restatement of richardson.py:111-125, same SciPy/NumPy calls,
+    including the reference's a*v term with a = 0 for the plain variant)."""
     A, f, sc, w = _W["A"], _W["f"], _W["scale"], _W["w"]
-    u, r, i0 = _W["u"], _W["r"], _W["i"]
+    u, v, r, i0 = _W["u"], _W["v"], _W["r"], _W["i"]
     t0 = time.perf_counter()
     for i in range(i0, i0 + k):
-        v = w[i % M] * (sc * r)
+        v = 0.0 * v + w[i % M] * (sc * r)
         u = u + v
         r = f - A.dot(u)
         float(np.linalg.norm(r))
-    _W.update(u=u, r=r, i=i0 + k)
+    _W.update(u=u, v=v, r=r, i=i0 + k)
     return time.perf_counter() - t0
 
 
@@ -206,12 +216,12 @@ def barrier(world):
 
 
 # ------------------------------------------------------------------ arms
-def config_dict(block_T):
+def config_dict():
     return {"workload": "cfg3: 8 anisotropic systems/GPU on 1024^2 cells (1023^2 unknowns), "
                         "weighted-Jacobi Richardson(32), Leja-ordered Chebyshev weights, f64",
             "systems_per_gpu": SYSTEMS_PER_GPU, "grid": N_SIDE - 1, "m": M,
             "step": "one outer sweep (32 inner updates) of every system",
-            "block_T": block_T, "l2": "no flush: per-GPU working set 3 x 67 MB > 126 MB L2",
+            "l2": "no flush: per-GPU working set 3 x 67 MB > 126 MB L2",
             "seed": 3}
 
 
@@ -233,7 +243,7 @@ def run_reference(args, rank, world):
     return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(None), "impl": "reference",
+            "config": config_dict(), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -360,10 +370,17 @@ def run_gpu(args, rank, world, local):
                              f"of the oracle port, {tc:.1f} s wall"}
             ref.close()
         traffic = _ncu_traffic(avg_T)
+        import bench_configs as BC
+        cpu_ttt = BC.cfg3_cpu_time_to_tol(cpu, ttt["inner_iterations"] if ttt else None, Pn) \
+            if world == 1 else None
+        dropin = None
+        if world == 1 and args.dropin:
+            dropin = BC.cfg3_dropin(None, wl, N_SIDE, TOL, MAX_OUTER_TOL)
+        configs = BC.run_all(ROOT) if (world == 1 and args.configs) else None
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic", "config": config_dict(block_T),
+               "data": "synthetic", "config": config_dict(), "block_T": block_T,
                "clocks": clk.summary(),
                "e2e": None if e2e_value is None else {"value": e2e_value, "unit": UNIT,
                        "h2d_bytes_per_step": int(F.nbytes), "d2h_bytes_per_step": int(F.nbytes),
@@ -391,7 +408,8 @@ def run_gpu(args, rank, world, local):
                                                    "point-step, halo recomputation included) "
                                                    "against SMs x 64 FP64 lanes x SM clock: "
                                                    "the limiting pipe of the blocked kernel"}},
-               "cpu_baseline": cpu, "time_to_tol": ttt}
+               "cpu_baseline": cpu, "time_to_tol": ttt, "cpu_time_to_tol": cpu_ttt,
+               "e2e_dropin": dropin, "configs": configs}
     return out
 
 
@@ -426,6 +444,10 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", dest="e2e_steps", type=int, default=2)
     ap.add_argument("--no-time-to-tol", dest="time_to_tol", action="store_false")  # kept for scripts
     ap.add_argument("--no-cpu", dest="no_cpu", action="store_true")
+    ap.add_argument("--no-configs", dest="configs", action="store_false",
+                    help="skip the per-config lines (cfg1, cfg2, cfg4, cfg5, NAG(16) sweep)")
+    ap.add_argument("--no-dropin", dest="dropin", action="store_false",
+                    help="skip the cfg3 reference-signature (CSR + numpy) e2e")
     ap.add_argument("--cpu-seconds", dest="cpu_seconds", type=float, default=10.0,
                     help="wall-time target of the bounded CPU baseline sample")
     args = ap.parse_args(argv)

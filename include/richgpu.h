@@ -122,6 +122,19 @@ int rg_matvec(const rg_op* A, const void* x, void* y, void* stream);
 int rg_residual(const rg_op* A, const void* u, const void* f, void* r,
                 double* norm2, void* stream);
 
+/* n_steps power-iteration steps (spectral.py:31-57, the loop body of
+ * _power_iteration) for every system of a float64 operator, one fused launch
+ * per step:  x = y_prev / ny_prev ;  y = A x  (shifted: y = sigma x - A x,
+ * spectral.py:75-76) ;  lam[k][b] = <x, y> ;  ny[k][b] = ||y||.
+ * Step 0 reads (y_prev, ny_prev) -- ny_prev NULL means y_prev already is the
+ * normalised start vector; step k > 0 reads the previous step's y and ny.
+ * y of step k goes to (k even ? y0 : y1); y_prev must not alias y0.
+ * x_last (may be NULL) receives x of the last step.  lam and ny are device
+ * arrays [n_steps][batch]. */
+int rg_power_steps(const rg_op* A, int n_steps, const double* y_prev, const double* ny_prev,
+                   double* y0, double* y1, double sigma, int shifted, double* lam,
+                   double* ny, double* x_last, void* stream);
+
 /* One inner update of _inner_update (richardson.py:49-59) for every system:
  *   plain/mom: r = f - A u ;  nag/nagex: r = f - A (u + at_i v)
  *   v_out = a_i v + w_i B^{-1} r ;  u_out = u + v_out

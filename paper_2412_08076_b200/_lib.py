@@ -52,6 +52,7 @@ _SIGS = [
     ("rg_op_destroy", _I, [_P]),
     ("rg_matvec", _I, [_P, _P, _P, _P]),
     ("rg_residual", _I, [_P, _P, _P, _P, _P, _P]),
+    ("rg_power_steps", _I, [_P, _I, _P, _P, _P, _P, C.c_double, _I, _P, _P, _P, _P]),
     ("rg_inner_update", _I, [_P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P, _P, _I, _P]),
     ("rg_tri_apply", _I, [_P, _I, C.c_double, _P, _P, _P, _P]),
     ("rg_unroll_adjoint_init", _I, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),

@@ -141,6 +141,25 @@ def cfg3(first=0, count=8, n=1024, m=32, seed=3):
     return dict(problems=probs, F=np.stack(F), schedules=scheds, scales=np.array(scales), m=m)
 
 
+def nag_sweep(first=0, count=8, n=1024, m=16):
+    """The north-star batched NAG(16) sweep at 1023^2: cfg3's systems
+    (default_rng(3)), NAG weights from cfg2's random-init MLP (same network
+    and seed, torch.manual_seed(2)) evaluated at each system's (lg eps, theta)."""
+    c3 = cfg3(first=first, count=count, n=n)
+    probs = c3["problems"]
+    torch.manual_seed(2)
+    net = _MLP(2, 2 * m).double()
+    mu = torch.tensor([[np.log10(p.epsilon), p.theta] for p in probs], dtype=torch.float64)
+    lo, hi = torch.tensor(ANISOTROPIC_BOUNDS[:, 0]), torch.tensor(ANISOTROPIC_BOUNDS[:, 1])
+    with torch.no_grad():
+        raw = net(2.0 * (mu - lo) / (hi - lo) - 1.0).numpy()
+    omega = np.log1p(np.exp(raw[:, :m]))
+    alpha = 1.0 / (1.0 + np.exp(-raw[:, m:]))
+    scheds = [WeightSchedule(omega=omega[b], alpha=alpha[b], variant="nag")
+              for b in range(len(probs))]
+    return dict(problems=probs, F=c3["F"], schedules=scheds, m=m)
+
+
 def fns_symbol(theta, eps, n, seed=4, scale=0.01, device="cuda"):
     """Random-init 4-layer conv net on the (n-1)^2 sine-frequency grid with
     channels (theta, eps, p/n, q/n) -> real symbol (fns.py:36: real), x scale."""
@@ -157,6 +176,16 @@ def fns_symbol(theta, eps, n, seed=4, scale=0.01, device="cuda"):
     with torch.no_grad():
         lam = net(x)[0, 0] * scale
     return lam.reshape(s * s).contiguous()
+
+
+def fns_symbol_portable(theta, eps, n, seed=4, scale=0.01):
+    """cfg4's conv-net symbol evaluated on the CPU and rounded to float32
+    (then widened back) as a NumPy array: the rounding absorbs last-bit
+    differences between BLAS builds, so the full-size goldens
+    (tests/golden/full_cfg4.npz) and the GPU test see the same bits on any
+    machine (the test checks the sha256)."""
+    lam = fns_symbol(theta, eps, n, seed=seed, scale=scale, device="cpu")
+    return lam.float().double().numpy()
 
 
 def cfg4(batch=4, n=1024, eps=1e-3, M=8, alternations=100, device="cuda"):

@@ -22,6 +22,7 @@
 #include "tri.cuh"
 #include "adjoint.cuh"
 #include "psweep.cuh"
+#include "power.cuh"
 
 using namespace rg;
 
@@ -592,6 +593,52 @@ int rg_residual(const rg_op* A, const void* u, const void* f, void* r, double* n
         if (e != cudaSuccess) rc = fail(RG_ECUDA, "reduce launch: %s", cudaGetErrorString(e));
     }
     if (norm2) CUDA_TRY(cudaFreeAsync(q.partials, st));
+    return rc;
+}
+
+int rg_power_steps(const rg_op* A, int n_steps, const double* y_prev, const double* ny_prev,
+                   double* y0, double* y1, double sigma, int shifted, double* lam, double* ny,
+                   double* x_last, void* stream) {
+    int rc = check_op(A);
+    if (rc) return rc;
+    if (A->d.dtype != RG_F64) return fail(RG_EUNSUPPORTED, "power steps run on float64 operators");
+    if (!y_prev || !y0 || !y1 || !lam || !ny) return fail(RG_ENULL, "null argument");
+    if (n_steps < 0) return fail(RG_EINVAL, "n_steps=%d", n_steps);
+    if ((const double*)y_prev == y0 || y0 == y1) return fail(RG_EINVAL, "y_prev / y0 / y1 alias");
+    if (n_steps == 0) return RG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const dim3 g((A->d.side + STEP_BX - 1) / STEP_BX, (A->d.side + STEP_BY - 1) / STEP_BY, A->d.batch);
+    const int ncta = g.x * g.y;
+    const int B = A->d.batch;
+    ensure_pool();
+    char* ws = nullptr;
+    const size_t part_bytes = sizeof(double) * 2 * (size_t)ncta * B;
+    CUDA_TRY(cudaMallocAsync((void**)&ws, part_bytes + sizeof(int) * B, st));
+    int* counter = (int*)(ws + part_bytes);
+    CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int) * B, st));
+    PowerArgs a;
+    a.A = view<double>(A);
+    a.sigma = sigma;
+    a.shifted = shifted ? 1 : 0;
+    a.part = (double*)ws;
+    a.ncta_cap = ncta;
+    a.counter = counter;
+    for (int k = 0; k < n_steps && rc == RG_OK; ++k) {
+        a.y_prev = k == 0 ? y_prev : ((k - 1) & 1 ? y1 : y0);
+        a.ny_prev = k == 0 ? ny_prev : ny + (size_t)(k - 1) * B;
+        a.y_out = (k & 1) ? y1 : y0;
+        a.x_out = k == n_steps - 1 ? x_last : nullptr;
+        a.lam_out = lam + (size_t)k * B;
+        a.ny_out = ny + (size_t)k * B;
+        switch (A->d.kind) {
+            case RG_CONST9: power_step_kernel<K_CONST9><<<g, dim3(STEP_BX, STEP_BY), 0, st>>>(a); break;
+            case RG_DIAG5: power_step_kernel<K_DIAG5><<<g, dim3(STEP_BX, STEP_BY), 0, st>>>(a); break;
+            default: power_step_kernel<K_VAR9><<<g, dim3(STEP_BX, STEP_BY), 0, st>>>(a); break;
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(RG_ECUDA, "power step launch: %s", cudaGetErrorString(e));
+    }
+    CUDA_TRY(cudaFreeAsync(ws, st));
     return rc;
 }
 

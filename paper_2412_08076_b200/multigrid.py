@@ -275,10 +275,26 @@ def build_hierarchy(A, n, coarsest=8, schedules=None, batch=1, device=None):
 def v_cycle(h: GpuHierarchy, f, u=None, pre=1, post=1):
     """multigrid.py:141-148: one V-cycle; numpy in -> numpy out."""
     host = _is_host(f)
-    ft = torch.as_tensor(np.asarray(f) if host else f).to(h.device, h.tdtype)
-    ut = None if u is None else torch.as_tensor(np.asarray(u) if _is_host(u) else u).to(
-        h.device, h.tdtype)
-    out = h.apply(ft, ut, pre, post)
+    ft = torch.as_tensor(np.asarray(f) if host else f)
+    ut = None if u is None else torch.as_tensor(np.asarray(u) if _is_host(u) else u)
+    cplx = ft.is_complex() or (ut is not None and ut.is_complex())
+    if cplx and not h.tdtype.is_complex:
+        # the reference promotes to complex (multigrid.py:144) and runs the
+        # real hierarchy on complex vectors.  Every operation of the cycle is
+        # real-linear with real coefficients, and (a + 0j) * x equals the
+        # component-wise real products, so the real and imaginary parts are
+        # two independent real V-cycles (same values as the promoted run).
+        ft = ft.to(torch.complex128)
+        ut = None if ut is None else ut.to(torch.complex128)
+        re = h.apply(ft.real.to(h.device, h.tdtype),
+                     None if ut is None else ut.real.to(h.device, h.tdtype), pre, post)
+        im = h.apply(ft.imag.to(h.device, h.tdtype),
+                     None if ut is None else ut.imag.to(h.device, h.tdtype), pre, post)
+        out = torch.complex(re, im)
+    else:
+        ft = ft.to(h.device, h.tdtype)
+        ut = None if ut is None else ut.to(h.device, h.tdtype)
+        out = h.apply(ft, ut, pre, post)
     shp = np.shape(f) if host else f.shape
     out = out.reshape(shp)
     return out.cpu().numpy() if host else out

@@ -25,7 +25,7 @@ import torch
 
 from . import _lib as L
 from .errors import DimensionMismatch, DivergenceError, SolveReport, UnsupportedOperator
-from .operator import GpuStencilOperator, as_operator, precond_scale
+from .operator import GpuStencilOperator, as_operator, operator_for_matrix, precond_scale
 from .precond import solve_tri, tri_spec, tri_inner_update
 
 INT_MAX = 2**31 - 1
@@ -368,7 +368,7 @@ def _op_for(A, f):
     dt = np.promote_types(getattr(A, "dtype", np.float64), fd)  # richardson.py:93
     if dt not in (np.float64, np.complex128):
         dt = np.dtype(np.float64)
-    return GpuStencilOperator.from_sparse(A, dtype=dt)
+    return operator_for_matrix(A, dtype=dt)
 
 
 def _check_len(op, x):

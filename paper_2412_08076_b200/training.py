@@ -96,6 +96,10 @@ class UnrollEngine:
         self.loss = torch.empty(B, dtype=torch.float64, device=dev)
         self.dots = torch.empty((max(self.K, 1), 3, B), dtype=torch.float64, device=dev)
         self.ds = None
+        # every forward overwrites the histories and the adjoint seeds, so a
+        # backward is only valid for the most recent forward: callers that
+        # keep a generation (UnrolledResidual) are checked against it
+        self.generation = 0
         if self.tri is not None:      # p_k = B^{-1} r_k history and scratch
             self.Pk = torch.empty((max(self.K, 1), B, n), dtype=torch.float64, device=dev)
             self.r = torch.empty_like(self.f)
@@ -135,17 +139,37 @@ class UnrollEngine:
             self.V[k + 1].copy_(self.V[k])
             L.check(lib.rg_precond_update(op.handle, sched, k % m, L.ptr(self.Pk[k]),
                                           L.ptr(self.U[k + 1]), L.ptr(self.V[k + 1]), None, s))
-        L.check(lib.rg_unroll_adjoint_init(op.handle, self.opT.handle, L.ptr(self.U[self.K]),
-                                           L.ptr(self.f), L.ptr(self.rbar), L.ptr(self.ubar),
-                                           L.ptr(self.vbar), L.ptr(self.loss), s))
+        self._adjoint_init()
+        self.generation += 1
         return self.loss
 
-    def backward(self):
+    def _adjoint_init(self):
+        """Loss and the adjoint seeds (rbar, ubar, vbar) from u_K."""
+        op = self.op
+        L.check(op._lib.rg_unroll_adjoint_init(op.handle, self.opT.handle, L.ptr(self.U[self.K]),
+                                               L.ptr(self.f), L.ptr(self.rbar), L.ptr(self.ubar),
+                                               L.ptr(self.vbar), L.ptr(self.loss),
+                                               L.stream_ptr()))
+
+    def backward(self, generation=None):
         """(d_omega, d_alpha, d_alpha_t) as host arrays [B, m] for the last
-        forward (each system's own loss)."""
+        forward (each system's own loss).  The reverse pass consumes the
+        adjoint seeds in place, so they are re-seeded from the stored u_K
+        first: repeated backward calls for one forward give the same
+        gradients.  `generation` (the value of self.generation right after
+        the forward in question) makes a stale backward raise instead of
+        silently differentiating a later forward."""
+        if self.ds is None:
+            raise RuntimeError("backward() before any forward()")
+        if generation is not None and generation != self.generation:
+            raise RuntimeError(
+                f"the unroll engine ran forward again (generation {self.generation}) after the "
+                f"forward being differentiated (generation {generation}); its histories are "
+                "overwritten -- use one engine per pending backward")
         op, m = self.op, self.ds.m
         lib, s = op._lib, L.stream_ptr()
         sched = C.byref(self.ds.struct)
+        self._adjoint_init()
         tkind = None
         if self.tri is not None:
             tkind = L.RG_TRI_SSOR_T if self.tri.mode == L.RG_TRI_SSOR else L.RG_TRI_SOR_T
@@ -216,13 +240,14 @@ class UnrolledResidual(torch.autograd.Function):
         to_np = lambda t: None if t is None else t.detach().cpu().numpy()  # noqa: E731
         loss = engine.forward(F, to_np(omega), to_np(alpha), to_np(alpha_t)).clone()
         ctx.engine = engine
+        ctx.generation = engine.generation
         ctx.devs = (omega.device, None if alpha is None else alpha.device,
                     None if alpha_t is None else alpha_t.device)
         return loss.to(omega.device)
 
     @staticmethod
     def backward(ctx, g):
-        dw, da, dat = ctx.engine.backward()
+        dw, da, dat = ctx.engine.backward(ctx.generation)
         gh = g.detach().cpu().numpy()[:, None]
         out = [torch.as_tensor(gh * x, dtype=torch.float64) for x in (dw, da, dat)]
         res = [out[0].to(ctx.devs[0])]
