@@ -46,12 +46,39 @@ def _deps_mtime() -> float:
     return max(f.stat().st_mtime for f in files)
 
 
-def _compile(src: Path, verbose: bool) -> tuple[Path, str]:
+def _includes(path: Path, seen=None) -> set:
+    """Local headers a source includes, transitively (#include "...")."""
+    seen = set() if seen is None else seen
+    for line in path.read_text().splitlines():
+        m = re.match(r'\s*#include\s+"([^"]+)"', line)
+        if m:
+            h = (path.parent / m.group(1)).resolve()
+            if h.exists() and h not in seen:
+                seen.add(h)
+                _includes(h, seen)
+    return seen
+
+
+def _stale(src: Path) -> bool:
+    """Object missing or older than its source or any header it includes."""
     obj = OBJ / (src.stem + ".o")
+    if not obj.exists() or not obj.with_suffix(".log").exists():
+        return True
+    newest = max([src.stat().st_mtime] + [h.stat().st_mtime for h in _includes(src)])
+    return obj.stat().st_mtime < newest
+
+
+def _compile(src: Path, force: bool) -> tuple[Path, str]:
+    """Compile one source unless its object is up to date; returns (object,
+    ptxas log of that object)."""
+    obj = OBJ / (src.stem + ".o")
+    if not force and not _stale(src):
+        return obj, obj.with_suffix(".log").read_text()
     cmd = [nvcc(), *ARCH, *CFLAGS, *EXTRA, "-c", str(src), "-o", str(obj)]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         raise RuntimeError(f"nvcc failed on {src.name}:\n{p.stderr}")
+    obj.with_suffix(".log").write_text(p.stderr)
     return obj, p.stderr
 
 
@@ -79,10 +106,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     OBJ.mkdir(parents=True, exist_ok=True)
     srcs = sorted(CSRC.glob("*.cu"))
+    flags = OBJ / ".flags"
+    force = force or not flags.exists() or flags.read_text() != " ".join(EXTRA)
     logs = []
     with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
         objs = []
-        for obj, log in ex.map(lambda s: _compile(s, verbose), srcs):
+        for obj, log in ex.map(lambda s: _compile(s, force), srcs):
             objs.append(obj)
             logs.append(log)
     tmp = LIB.with_suffix(".so.tmp")
@@ -92,6 +121,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if p.returncode != 0:
         raise RuntimeError(f"link failed:\n{p.stderr}")
     os.replace(tmp, LIB)
+    flags.write_text(" ".join(EXTRA))
     log = "\n".join(logs)
     (PKG / "build" / "ptxas.log").write_text(log)
     if verbose:

@@ -23,6 +23,7 @@
 #include "adjoint.cuh"
 #include "psweep.cuh"
 #include "power.cuh"
+#include "wave.cuh"
 
 using namespace rg;
 
@@ -80,6 +81,8 @@ struct rg_solver {
     int check;
     int block_T;
     bool use_block;
+    bool use_wave;    // plain sweeps take the wavefront kernel (wave.cuh)
+    int wave_L;       // its segment rows
     bool use_small;   // whole solve in one launch (grid fits in shared memory)
     bool small_done;  // that launch has been queued
     int cl_nc, cl_rows, cl_ppt;   // cluster shape of the resident solver
@@ -191,10 +194,64 @@ static int step1(const rg_op* A, const StepReq& q, cudaStream_t st) {
     return fail(RG_EINVAL, "bad dtype %d", A->d.dtype);
 }
 
+// wavefront sweep tuning (env overrides for measurement: RG_WAVE=0 disables,
+// RG_WAVE_T sets the default depth, RG_WAVE_L the segment rows)
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+static int wave_seg_rows() {   // read per solver (measurement scripts vary it in-process)
+    const int L = env_int("RG_WAVE_L", RG_WV_L);
+    return L < 8 ? 8 : L;
+}
+static bool wave_enabled() { return env_int("RG_WAVE", 1) != 0; }
+constexpr int WV_MIN_SIDE = 128;
+
 // ------------------------------------------------------- block dispatch
+template <typename S>
+static int do_wave(rg_solver* S_, int T, cudaStream_t st) {
+    const rg_op* A = S_->A;
+    static thread_local WaveArgs<S> a;   // ~5 KB of kernel parameters
+    a.side = A->d.side;
+    a.P = A->P;
+    a.u_in = (const S*)S_->u[S_->cur];
+    a.u_out = (S*)S_->u[S_->cur ^ 1];
+    a.f = (const S*)S_->f;
+    a.omega = S_->s.omega;
+    a.m = S_->s.m;
+    a.k0 = (int)S_->k;
+    a.seg_rows = S_->wave_L;
+    wave_ntiles(A->d.side, T, a.seg_rows, &a.nstrip);
+    const bool jac = S_->s.precond == RG_PRECOND_JACOBI_SCALAR;
+    EpiArgs& e = a.epi;
+    e.st = S_->d_st;
+    e.trace = S_->d_trace;
+    e.trace_stride = S_->trace_stride;
+    e.partials = S_->d_part;
+    e.ncta_cap = S_->ncta_cap;
+    e.cfg = S_->cfg;
+    e.j0 = (int)S_->k;
+    e.nslots = T;
+    e.with_f = 0;
+    e.buf = S_->cur;
+    const int B = A->d.batch;
+    for (int b0 = 0; b0 < B; b0 += BLK_MAXB) {
+        const int nsys = B - b0 < BLK_MAXB ? B - b0 : BLK_MAXB;
+        a.b0 = b0;
+        for (int j = 0; j < nsys; ++j) {
+            for (int d = 0; d < 9; ++d) a.coef[j][d] = A->hcoef[(size_t)(b0 + j) * 9 + d];
+            a.scale[j] = jac ? S_->hscale[b0 + j] : 0.0;
+        }
+        cudaError_t err = launch_wave<S>(a, T, jac, nsys, st);
+        if (err != cudaSuccess) return fail(RG_ECUDA, "wave sweep launch: %s", cudaGetErrorString(err));
+    }
+    return RG_OK;
+}
+
 template <typename S>
 static int do_block(rg_solver* S_, int T, int norm_first_u, cudaStream_t st) {
     const rg_op* A = S_->A;
+    if (S_->use_wave && T <= WV_TMAX) return do_wave<S>(S_, T, st);
     static thread_local BlockArgs<S> a;   // ~5 KB of kernel parameters
     a.side = A->d.side;
     a.P = A->P;
@@ -1309,8 +1366,13 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     const bool real = A->d.dtype == RG_F32 || A->d.dtype == RG_F64;
     S->use_block = real && A->d.kind == RG_CONST9 && check == RG_CHECK_OUTER &&
                    s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
-    // automatic depth: measured optimum on B200 for the 64x64 tile (profiles/)
-    S->block_T = block_T != 0 ? block_T : 5;
+    S->use_wave = S->use_block && s->variant == RG_PLAIN && A->d.side >= WV_MIN_SIDE &&
+                  wave_enabled();
+    S->wave_L = wave_seg_rows();
+    // automatic depth: measured optima on B200 (profiles/): 5 for the 64x64
+    // overlapped tile, 4 for the wavefront strip
+    S->block_T = block_T != 0 ? block_T : (S->use_wave ? env_int("RG_WAVE_T", 4) : 5);
+    if (S->block_T > 8) S->block_T = 8;
     if (!S->use_block) S->block_T = 1;
     {
         // resident cluster solver: the whole solve in one launch when the grid
@@ -1332,6 +1394,10 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     for (int T = 1; T <= 8; ++T) {
         const int nt = block_ntiles(A->d.side, T, nullptr);
         if (nt > cap) cap = nt;
+        if (T <= WV_TMAX) {
+            const int nw = wave_ntiles(A->d.side, T, S->wave_L, nullptr);
+            if (nw > cap) cap = nw;
+        }
     }
     S->ncta_cap = cap;
     S->trace_stride = max_outer + 1;

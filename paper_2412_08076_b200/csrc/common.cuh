@@ -99,6 +99,8 @@ __device__ __forceinline__ void cp_async_el(void* sdst, const void* gsrc, bool v
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // ---- per-system solver state (device) ------------------------------------
 // Mirrors the local variables of solve_stationary (richardson.py:92-136).
