@@ -264,7 +264,7 @@ def run_gpu(args, rank, world, local):
 
     # ---- device-resident timed sweeps
     S = G.StationarySolver(op, scheds, P, tol=1e-300, max_outer=10**7, block_T=args.block_T)
-    S.begin(F)
+    S.begin(F_dev(op, F))
     stream = torch.cuda.current_stream()
     launches_per_step = None
     for _ in range(args.warmup):
@@ -274,24 +274,27 @@ def run_gpu(args, rank, world, local):
             steps += S.step()
         launches_per_step = S.info()[2] - n0
     torch.cuda.synchronize()
-    block_T = S.info()[1]
+    kernel, block_T, seg_rows = S.plan()
+    # one CUDA event pair per step (sweep); the launches of a sweep are
+    # back to back on the stream, so a sweep's duration / its launches is
+    # the average launch duration of the dominant kernel
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps * launches_per_step)]
-    k_launch = [0] * len(ev)
+          for _ in range(args.steps)]
+    chunk_T = []
     barrier(world)
     torch.cuda.synchronize()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         start.record(stream)
-        e = 0
-        for _ in range(args.steps):
+        for i in range(args.steps):
+            ev[i][0].record(stream)
             steps = 0
             while steps < M:
-                ev[e][0].record(stream)
-                k_launch[e] = S.step()
-                ev[e][1].record(stream)
-                steps += k_launch[e]
-                e += 1
+                k = S.step()
+                if i == 0:
+                    chunk_T.append(k)
+                steps += k
+            ev[i][1].record(stream)
         stop.record(stream)
         torch.cuda.synchronize()
     barrier(world)
@@ -299,27 +302,21 @@ def run_gpu(args, rank, world, local):
     t = max_over_ranks(t_local, world)
     upd_step = B * Pn * M
     value = world * upd_step * args.steps / t
-    # dominant kernel: the temporally blocked sweep (every launch of the step;
-    # a 32-step sweep runs as balanced chunks, e.g. 6,6,5,5,5,5 at T=5)
-    dur = np.array([ev[i][0].elapsed_time(ev[i][1]) / 1e3 for i in range(e)])
-    steps_l = np.array(k_launch[:e], dtype=float)
-    avg = float(dur.mean())
-    avg_T = float(steps_l.mean())
+    e = args.steps * launches_per_step                     # our kernel launches in the region
+    dur = np.array([ev[i][0].elapsed_time(ev[i][1]) / 1e3 for i in range(args.steps)])
+    avg = float(dur.sum() / e)                             # average launch duration
+    avg_T = float(M / launches_per_step)
     alg_bytes = BYTES_PER_UPDATE * B * Pn * avg_T          # per launch (average)
-    achieved = float(BYTES_PER_UPDATE * B * Pn * steps_l.sum() / dur.sum() / 1e9)
+    achieved = alg_bytes / avg / 1e9
     peak = _peak_hbm()
     share = float(dur.sum() / t_local)
-    # the bound that actually limits the blocked kernel: FP64 issue.  Every
-    # launch computes its whole 64 x 64 windows (owned points + T-cell halo)
-    # T times, 22 FP64 instructions per point-step (11 DMUL + 10 DADD + 1
-    # DFMA: the reference's unfused CSR-order sum, SASS-counted).
+    # the bound that actually limits the sweep: FP64 issue.  22 FP64
+    # instructions per COMPUTED point-step (11 DMUL + 10 DADD + 1 DFMA: the
+    # reference's unfused CSR-order sum, SASS-counted), halo recomputation
+    # of the kernel's tiling included
     side = N_SIDE - 1
-    computed = 0.0
-    for T_, d_ in zip(steps_l, dur):
-        T_ = int(T_)
-        tiles = (-(-side // (64 - 2 * T_))) ** 2   # block_ntiles: ceil(side / (64 - 2T))^2
-        computed += tiles * 64 * 64 * T_ * B
-    fp64_rate = computed * FP64_PER_POINT_STEP / float(dur.sum())
+    computed = sum(_computed_point_steps(kernel, side, T_, seg_rows) for T_ in chunk_T) * B
+    fp64_rate = computed * FP64_PER_POINT_STEP / (float(dur.sum()) / args.steps)
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp64_peak = n_sm * 64 * (clk.summary().get("sm_mhz") or 1965.0) * 1e6
 
@@ -380,7 +377,7 @@ def run_gpu(args, rank, world, local):
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic", "config": config_dict(), "block_T": block_T,
+               "data": "synthetic", "config": config_dict(), "block_T": block_T, "kernel": kernel,
                "clocks": clk.summary(),
                "e2e": None if e2e_value is None else {"value": e2e_value, "unit": UNIT,
                        "h2d_bytes_per_step": int(F.nbytes), "d2h_bytes_per_step": int(F.nbytes),
@@ -391,8 +388,7 @@ def run_gpu(args, rank, world, local):
                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak["value"],
                             "unit": "GB/s", "frac": achieved / peak["value"],
                             "traffic": traffic, "peak_source": peak["source"],
-                            "kernel": f"block_kernel<double,plain,T~{block_T}> (chunks "
-                                      f"{sorted(set(int(x) for x in steps_l))})",
+                            "kernel": _kernel_name(kernel, block_T, seg_rows, chunk_T),
                             "algorithmic_bytes_per_launch": alg_bytes,
                             "avg_steps_per_launch": avg_T,
                             "avg_launch_s": avg, "kernel_share_of_step": share,
@@ -403,7 +399,7 @@ def run_gpu(args, rank, world, local):
                                            "peak_Tinst_s": fp64_peak / 1e12,
                                            "frac": fp64_rate / fp64_peak,
                                            "computed_point_steps_per_owned": computed / (
-                                               B * Pn * float(steps_l.sum())),
+                                               B * Pn * float(M)),
                                            "note": "FP64 instructions issued (22 per computed "
                                                    "point-step, halo recomputation included) "
                                                    "against SMs x 64 FP64 lanes x SM clock: "
@@ -411,6 +407,36 @@ def run_gpu(args, rank, world, local):
                "cpu_baseline": cpu, "time_to_tol": ttt, "cpu_time_to_tol": cpu_ttt,
                "e2e_dropin": dropin, "configs": configs}
     return out
+
+
+def F_dev(op, F):
+    return op.to_device(F)
+
+
+def _computed_point_steps(kernel, side, T, seg_rows):
+    """Point-steps one launch of T fused steps computes for ONE system
+    (owned points plus the recomputed halo of the kernel's tiling)."""
+    if kernel == "wave":
+        W = 128                                   # csrc/wave.cuh: 32 lanes x 4 columns
+        nstrip = -(-side // (W - 2 * T))
+        total = 0
+        for r0 in range(0, side, seg_rows):
+            L = min(seg_rows, side - r0)
+            total += sum(W * (L + 2 * T - 2 * t) for t in range(1, T + 1))
+        return nstrip * total
+    if kernel == "tile":
+        tiles = (-(-side // (64 - 2 * T))) ** 2   # block_ntiles: 64 x 64 windows
+        return tiles * 64 * 64 * T
+    return side * side * T
+
+
+def _kernel_name(kernel, T, seg_rows, chunks):
+    if kernel == "wave":
+        return (f"wave_kernel<double,T={T},Jacobi> (csrc/wave.cuh: 128-column strips x "
+                f"{seg_rows}-row segments, chunks {sorted(set(chunks))})")
+    if kernel == "tile":
+        return f"block_kernel<double,plain,T~{T}> (chunks {sorted(set(chunks))})"
+    return kernel
 
 
 def _peak_hbm():
@@ -422,11 +448,11 @@ def _peak_hbm():
 
 
 def _ncu_traffic(avg_T):
-    """DRAM bytes per (average) launch of the dominant kernel, from the
-    committed ncu capture (profiles/ncu_block_kernel.json: read + write per
-    launch of a T-step launch; traffic is ~independent of T since u and f are
-    read once and u written once per launch), or None."""
-    p = ROOT / "profiles" / "ncu_block_kernel.json"
+    """DRAM bytes per launch of the dominant kernel, from the committed ncu
+    capture (profiles/ncu_wave_kernel.json: read + write of one T = 4
+    launch: u and f read once, u written once, plus the strip / segment
+    halos), or None."""
+    p = ROOT / "profiles" / "ncu_wave_kernel.json"
     try:
         d = json.loads(p.read_text())
         return float(d["dram_bytes_per_launch"])

@@ -290,6 +290,13 @@ int rg_solver_report(const rg_solver* S, int b, rg_report* out);
 /* Copy trace[0..iterations] of system b into host buffer out (cap entries). */
 int rg_solver_trace(const rg_solver* S, int b, double* out, int cap,
                     int* n_out);
+/* The sweep kernel a solver uses (for measurement and reporting):
+ * kernel = RG_KERNEL_STEP (one inner step per launch), RG_KERNEL_TILE
+ * (overlapped-tile temporal blocking), RG_KERNEL_WAVE (wavefront strips,
+ * seg_rows rows per segment) or RG_KERNEL_CLUSTER (the whole solve in one
+ * launch); block_T = inner steps fused per launch. */
+enum { RG_KERNEL_STEP = 0, RG_KERNEL_TILE = 1, RG_KERNEL_WAVE = 2, RG_KERNEL_CLUSTER = 3 };
+int rg_solver_plan(const rg_solver* S, int* kernel, int* block_T, int* seg_rows);
 /* Inner steps queued so far and the temporal-blocking depth in use. */
 int rg_solver_info(const rg_solver* S, long long* steps_queued,
                    int* block_T, int* launches);

@@ -20,6 +20,8 @@ RG_PRECOND_NONE, RG_PRECOND_JACOBI_SCALAR, RG_PRECOND_JACOBI_FIELD = 0, 1, 2
 RG_CHECK_OUTER, RG_CHECK_INNER = 0, 1
 RG_TRI_SOR, RG_TRI_SSOR, RG_TRI_SOR_T, RG_TRI_SSOR_T = 1, 2, 3, 4
 RG_ACTIVE, RG_CONVERGED, RG_DIVERGED, RG_MAXED = 0, 1, 2, 3
+RG_KERNEL_STEP, RG_KERNEL_TILE, RG_KERNEL_WAVE, RG_KERNEL_CLUSTER = 0, 1, 2, 3
+KERNEL_NAMES = {0: "step", 1: "tile", 2: "wave", 3: "cluster"}
 RG_OK, RG_EINVAL, RG_ESIZE, RG_ENULL, RG_EUNSUPPORTED, RG_ECUDA, RG_ESTATE = 0, -1, -2, -3, -4, -5, -6
 
 VARIANT_CODE = {"plain": RG_PLAIN, "mom": RG_MOM, "nag": RG_NAG, "nagex": RG_NAGEX}
@@ -81,6 +83,7 @@ _SIGS = [
     ("rg_solver_poll", _I, [_P, _P, C.POINTER(_I), C.POINTER(_I)]),
     ("rg_solver_report", _I, [_P, _I, C.POINTER(rg_report)]),
     ("rg_solver_trace", _I, [_P, _I, C.POINTER(C.c_double), _I, C.POINTER(_I)]),
+    ("rg_solver_plan", _I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     ("rg_solver_info", _I, [_P, C.POINTER(C.c_longlong), C.POINTER(_I), C.POINTER(_I)]),
 ]
 SYMBOLS = [s[0] for s in _SIGS]

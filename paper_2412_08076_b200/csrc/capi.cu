@@ -200,9 +200,25 @@ static int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return (v && *v) ? atoi(v) : dflt;
 }
-static int wave_seg_rows() {   // read per solver (measurement scripts vary it in-process)
-    const int L = env_int("RG_WAVE_L", RG_WV_L);
-    return L < 8 ? 8 : L;
+// Segment rows of the wavefront sweep for a batch, or 0 when the grid gives
+// too few strips x segments to fill the GPU (one-warp CTAs, 8 resident per
+// SM at ~206 registers): then the overlapped-tile kernel, which cuts a system
+// into ~4x more CTAs, is faster.  Measured on cfg3's 1023^2 systems
+// (profiles/wave_batch_r02.json): 8 systems L = 64 352 vs tile 279 G upd/s;
+// 4 systems L = 32 279 vs 250; 1-2 systems the tile kernel wins.
+// RG_WAVE_L overrides (read per solver, so measurement scripts vary it).
+static int wave_seg_rows(int side, int batch) {
+    const int forced = env_int("RG_WAVE_L", 0);
+    if (forced > 0) return forced < 8 ? 8 : forced;
+    int dev = 0, nsm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long slots = 8ll * nsm;
+    for (int L = RG_WV_L; L >= 32; L /= 2) {
+        int nstrip = 0;
+        const long long n = (long long)batch * wave_ntiles(side, 4, L, &nstrip);
+        if (n * 100 >= slots * 85) return L;
+    }
+    return 0;
 }
 static bool wave_enabled() { return env_int("RG_WAVE", 1) != 0; }
 constexpr int WV_MIN_SIDE = 128;
@@ -1366,9 +1382,9 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     const bool real = A->d.dtype == RG_F32 || A->d.dtype == RG_F64;
     S->use_block = real && A->d.kind == RG_CONST9 && check == RG_CHECK_OUTER &&
                    s->precond != RG_PRECOND_JACOBI_FIELD && block_T != 1;
+    S->wave_L = wave_seg_rows(A->d.side, A->d.batch);
     S->use_wave = S->use_block && s->variant == RG_PLAIN && A->d.side >= WV_MIN_SIDE &&
-                  wave_enabled();
-    S->wave_L = wave_seg_rows();
+                  wave_enabled() && S->wave_L > 0;
     // automatic depth: measured optima on B200 (profiles/): 5 for the 64x64
     // overlapped tile, 4 for the wavefront strip
     S->block_T = block_T != 0 ? block_T : (S->use_wave ? env_int("RG_WAVE_T", 4) : 5);
@@ -1394,7 +1410,7 @@ int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double 
     for (int T = 1; T <= 8; ++T) {
         const int nt = block_ntiles(A->d.side, T, nullptr);
         if (nt > cap) cap = nt;
-        if (T <= WV_TMAX) {
+        if (S->use_wave && T <= WV_TMAX) {
             const int nw = wave_ntiles(A->d.side, T, S->wave_L, nullptr);
             if (nw > cap) cap = nw;
         }
@@ -1655,6 +1671,17 @@ int rg_solver_trace(const rg_solver* S, int b, double* out, int cap, int* n_out)
     CUDA_TRY(cudaMemcpy(out, S->d_trace + (size_t)b * S->trace_stride, sizeof(double) * n,
                         cudaMemcpyDeviceToHost));
     if (n_out) *n_out = n;
+    return RG_OK;
+}
+
+int rg_solver_plan(const rg_solver* S, int* kernel, int* block_T, int* seg_rows) {
+    if (!S) return fail(RG_ENULL, "null solver");
+    if (kernel)
+        *kernel = S->use_small ? RG_KERNEL_CLUSTER
+                  : !S->use_block ? RG_KERNEL_STEP
+                  : (S->use_wave && S->block_T <= WV_TMAX) ? RG_KERNEL_WAVE : RG_KERNEL_TILE;
+    if (block_T) *block_T = S->block_T;
+    if (seg_rows) *seg_rows = S->use_wave ? S->wave_L : 0;
     return RG_OK;
 }
 

@@ -221,6 +221,12 @@ class StationarySolver:
         L.check(self.lib.rg_solver_poll(self._h, L.stream_ptr(), C.byref(act), C.byref(done)))
         return act.value, bool(done.value)
 
+    def plan(self):
+        """(kernel name, steps fused per launch, wave segment rows)."""
+        kind, T, rows = C.c_int(), C.c_int(), C.c_int()
+        L.check(self.lib.rg_solver_plan(self._h, C.byref(kind), C.byref(T), C.byref(rows)))
+        return L.KERNEL_NAMES[kind.value], T.value, rows.value
+
     def info(self):
         k, T, nl = C.c_longlong(), C.c_int(), C.c_int()
         L.check(self.lib.rg_solver_info(self._h, C.byref(k), C.byref(T), C.byref(nl)))

@@ -25,9 +25,10 @@ ap.add_argument("--T", default="4")
 ap.add_argument("--L", default="64")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--out", default=None)
+ap.add_argument("--batch", type=int, default=8)
 args = ap.parse_args()
 
-wl = CF.cfg3()
+wl = CF.cfg3(count=args.batch)
 op = G.GpuStencilOperator.from_problems(wl["problems"])
 P = [G.JacobiScale(np.float64(s)) for s in wl["scales"]]
 Fd = op.to_device(wl["F"])
@@ -51,7 +52,7 @@ def measure(T, env):
         S.run_sweeps(20)
         e1.record()
         torch.cuda.synchronize()
-        out.append(8 * 1023 ** 2 * 32 * 20 / (e0.elapsed_time(e1) / 1e3) / 1e9)
+        out.append(args.batch * 1023 ** 2 * 32 * 20 / (e0.elapsed_time(e1) / 1e3) / 1e9)
     del S, S4
     return out, sha
 
