@@ -205,6 +205,18 @@ int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void*
 int rg_mgs_arnoldi(int dtype, int batch, int n, void* w, long long ldw, const void* V,
                    long long ldv, int k, void* H, double* wnorm2, void* stream);
 
+/* Tail of an Arnoldi step (fgmres.py:79-80,106-107) for `batch` systems at
+ * index k: hk1 = sqrt(wnorm2[b]); vnext_b = w_b / hk1; hcol[b][0..k+1] =
+ * (H[0..k][b], hk1) packed for one device->host copy.  vnext is computed
+ * unconditionally (the host ignores it after a stop). */
+int rg_arnoldi_tail(int dtype, int batch, int n, const void* w, long long ldw, void* vnext,
+                    long long ldv, const void* H, int k, const double* wnorm2, void* hcol,
+                    void* stream);
+/* u += Z[:, :k] y for one system (fgmres.py:119); Z column j at Z + j*ldz
+ * elements, y device [k]. */
+int rg_krylov_update(int dtype, int n, void* u, const void* Z, long long ldz, const void* y, int k,
+                     void* stream);
+
 /* ---- Gauss-Seidel / SOR / SSOR preconditioners (precond.py:79-118) --------
  * z = B^{-1} r for every system of a CONST9 real operator:
  *   RG_TRI_SOR  : z = relax (D + relax L)^{-1} r          (gauss_seidel: relax 1)

@@ -74,6 +74,8 @@ _SIGS = [
     ("rg_mgs_step", _I, [_I, _I, _I, _P, C.c_longlong, _P, C.c_longlong, _P, _P, C.c_longlong, _P,
                          _P, _P]),
     ("rg_mgs_arnoldi", _I, [_I, _I, _I, _P, C.c_longlong, _P, C.c_longlong, _I, _P, _P, _P]),
+    ("rg_arnoldi_tail", _I, [_I, _I, _I, _P, C.c_longlong, _P, C.c_longlong, _P, _I, _P, _P, _P]),
+    ("rg_krylov_update", _I, [_I, _I, _P, _P, C.c_longlong, _P, _I, _P]),
     ("rg_solver_create", _I, [C.POINTER(_P), _P, C.POINTER(rg_sched), C.c_double, _I, _I, _I]),
     ("rg_solver_destroy", _I, [_P]),
     ("rg_solver_begin", _I, [_P, _P, _P, _P, _P, _P, _P]),

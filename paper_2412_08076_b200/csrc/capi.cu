@@ -1327,12 +1327,14 @@ int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void*
     const dim3 g(ncta, batch);
     if (dtype == RG_F64) {
         MgsArgs<double> a{(double*)w, ldw, (const double*)v, ldv, (const double*)h,
-                          (const double*)vn, ldvn, part, n, wnorm2 != nullptr};
+                          (const double*)vn, ldvn, part, n, wnorm2 != nullptr,
+                          nullptr, nullptr, nullptr};
         mgs_kernel<double><<<g, MGS_NT, 0, st>>>(a);
         mgs_finish_kernel<double><<<batch, MGS_NT, 0, st>>>(part, ncta, (double*)hn, wnorm2);
     } else {
         MgsArgs<double2> a{(double2*)w, ldw, (const double2*)v, ldv, (const double2*)h,
-                           (const double2*)vn, ldvn, part, n, wnorm2 != nullptr};
+                           (const double2*)vn, ldvn, part, n, wnorm2 != nullptr,
+                           nullptr, nullptr, nullptr};
         mgs_kernel<double2><<<g, MGS_NT, 0, st>>>(a);
         mgs_finish_kernel<double2><<<batch, MGS_NT, 0, st>>>(part, ncta, (double2*)hn, wnorm2);
     }
@@ -1342,20 +1344,153 @@ int rg_mgs_step(int dtype, int batch, int n, void* w, long long ldw, const void*
     return RG_OK;
 }
 
+}  // extern "C"
+
+// Whole MGS orthogonalisation (fgmres.py:76-78): k + 2 fused passes per
+// system.  Systems are processed in chunks small enough that a chunk's w
+// plus the two basis vectors a pass touches stay resident in L2 (126 MB),
+// so a pass streams only the next basis vector from HBM; each pass is ONE
+// launch (the partial sums are finished by the last CTA of each system).
+// Persistent single-launch MGS when a CTA per SM can hold its slices of w
+// and of the basis vector in shared memory (cooperative launch for
+// guaranteed co-residency); returns -1 when it does not apply.
+template <typename S>
+static int mgs_persist(int batch, int n, S* w, long long ldw, const S* V, long long ldv, int k,
+                       S* H, double* wnorm2, cudaStream_t st) {
+    if (env_int("RG_MGS_PERSIST", 1) == 0) return -1;
+    int dev = 0, nsm = 0, coop = 0, smem_optin = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (!coop || nsm < 1) return -1;
+    const int slice = (n + nsm - 1) / nsm;
+    const size_t smem = 2 * (size_t)slice * sizeof(S);
+    if (smem + 1024 > (size_t)smem_optin || slice > MGSP_NT * MGSP_R) return -1;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(mgs_persist_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(smem_optin - 1024)) != cudaSuccess)
+            return -1;
+        attr = true;
+    }
+    char* ws = nullptr;
+    const size_t part_bytes = sizeof(double) * 3 * 2 * (size_t)nsm;   // two parities
+    ensure_pool();
+    if (cudaMallocAsync((void**)&ws, part_bytes + 2 * sizeof(unsigned int), st) != cudaSuccess) return -1;
+    unsigned int* cnt = (unsigned int*)(ws + part_bytes);
+    if (cudaMemsetAsync(cnt, 0, 2 * sizeof(unsigned int), st) != cudaSuccess) return -1;
+    MgsPArgs<S> a;
+    a.w = w; a.ldw = ldw; a.V = V; a.ldv = ldv; a.H = H; a.wnorm2 = wnorm2;
+    a.part = (double*)ws; a.bar.count = cnt; a.bar.gen = cnt + 1;
+    a.n = n; a.k = k; a.B = batch; a.slice = slice;
+    void* args[] = {&a};
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)mgs_persist_kernel<S>, dim3(nsm),
+                                                dim3(MGSP_NT), args, smem, st);
+    cudaFreeAsync(ws, st);
+    if (e != cudaSuccess) {        // e.g. co-residency refused: take the multi-launch path
+        cudaGetLastError();
+        return -1;
+    }
+    return RG_OK;
+}
+
+template <typename S>
+static int mgs_arnoldi_t(int batch, int n, S* w, long long ldw, const S* V, long long ldv, int k,
+                         S* H, double* wnorm2, cudaStream_t st) {
+    {
+        const int rc = mgs_persist<S>(batch, n, w, ldw, V, ldv, k, H, wnorm2, st);
+        if (rc != -1) return rc;
+    }
+    int ncta = (n + MGS_NT * 4 - 1) / (MGS_NT * 4);
+    if (ncta > 1024) ncta = 1024;
+    const double L2_BUDGET = (double)env_int("RG_MGS_L2MB", 96) * 1024 * 1024;
+    int chunk = (int)(L2_BUDGET / (3.0 * (double)n * sizeof(S)));
+    if (chunk < 1) chunk = 1;
+    if (chunk > batch) chunk = batch;
+    char* ws = nullptr;
+    const size_t part_bytes = sizeof(double) * 3 * (size_t)ncta * batch;
+    ensure_pool();
+    CUDA_TRY(cudaMallocAsync((void**)&ws, part_bytes + sizeof(int) * batch, st));
+    int* counter = (int*)(ws + part_bytes);
+    CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(int) * batch, st));
+    auto vi = [&](int i) { return V + (size_t)i * n; };
+    auto hi = [&](int i) { return H + (size_t)i * batch; };
+    for (int b0 = 0; b0 < batch; b0 += chunk) {
+        const int nb = batch - b0 < chunk ? batch - b0 : chunk;
+        const dim3 g(ncta, nb);
+        for (int i = 0; i <= k + 1; ++i) {
+            // pass i: w -= h_{i-1} v_{i-1} ; h_i = <v_i, w>  (last pass: ||w||^2)
+            const bool last = i == k + 1;
+            MgsArgs<S> a{w + b0 * ldw, ldw,
+                         i ? vi(i - 1) + b0 * ldv : nullptr, ldv,
+                         i ? hi(i - 1) + b0 : nullptr,
+                         last ? nullptr : vi(i) + b0 * ldv, ldv,
+                         (double*)ws + (size_t)3 * ncta * b0, n, last ? 1 : 0,
+                         counter + b0, last ? nullptr : hi(i) + b0, last ? wnorm2 + b0 : nullptr};
+            mgs_kernel<S><<<g, MGS_NT, 0, st>>>(a);
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(ws, st);
+    if (e != cudaSuccess) return fail(RG_ECUDA, "mgs launch: %s", cudaGetErrorString(e));
+    return RG_OK;
+}
+
+extern "C" {
+
 int rg_mgs_arnoldi(int dtype, int batch, int n, void* w, long long ldw, const void* V, long long ldv,
                    int k, void* H, double* wnorm2, void* stream) {
     if (!w || !V || !H || !wnorm2) return fail(RG_ENULL, "null argument");
     if (k < 0) return fail(RG_EINVAL, "k must be >= 0");
-    const size_t el = dtype == RG_C128 ? sizeof(double2) : sizeof(double);
-    auto vi = [&](int i) { return (const void*)((const char*)V + (size_t)i * n * el); };
-    auto hi = [&](int i) { return (void*)((char*)H + (size_t)i * batch * el); };
-    // step i applies the projection on v_{i-1} and takes <v_i, w> (:76-78)
-    for (int i = 0; i <= k; ++i) {
-        const int rc = rg_mgs_step(dtype, batch, n, w, ldw, i ? vi(i - 1) : nullptr, ldv,
-                                   i ? hi(i - 1) : nullptr, vi(i), ldv, hi(i), nullptr, stream);
-        if (rc) return rc;
-    }
-    return rg_mgs_step(dtype, batch, n, w, ldw, vi(k), ldv, hi(k), nullptr, 0, nullptr, wnorm2, stream);
+    if (dtype != RG_F64 && dtype != RG_C128) return fail(RG_EINVAL, "mgs: float64 or complex128");
+    if (batch < 1 || n < 1) return fail(RG_ESIZE, "bad size");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == RG_F64)
+        return mgs_arnoldi_t<double>(batch, n, (double*)w, ldw, (const double*)V, ldv, k, (double*)H,
+                                     wnorm2, st);
+    return mgs_arnoldi_t<double2>(batch, n, (double2*)w, ldw, (const double2*)V, ldv, k, (double2*)H,
+                                  wnorm2, st);
+}
+
+int rg_arnoldi_tail(int dtype, int batch, int n, const void* w, long long ldw, void* vnext,
+                    long long ldv, const void* H, int k, const double* wnorm2, void* hcol,
+                    void* stream) {
+    if (!w || !vnext || !H || !wnorm2 || !hcol) return fail(RG_ENULL, "null argument");
+    if (dtype != RG_F64 && dtype != RG_C128) return fail(RG_EINVAL, "arnoldi: float64 or complex128");
+    if (batch < 1 || n < 1 || k < 0) return fail(RG_ESIZE, "bad size");
+    cudaStream_t st = (cudaStream_t)stream;
+    int nx = (n + MGS_NT * 4 - 1) / (MGS_NT * 4);
+    if (nx > 256) nx = 256;
+    const dim3 g(nx, batch);
+    if (dtype == RG_F64)
+        arnoldi_tail_kernel<double><<<g, MGS_NT, 0, st>>>((const double*)w, ldw, (double*)vnext,
+                                                          ldv, (const double*)H, k, wnorm2,
+                                                          (double*)hcol, n);
+    else
+        arnoldi_tail_kernel<double2><<<g, MGS_NT, 0, st>>>((const double2*)w, ldw, (double2*)vnext,
+                                                           ldv, (const double2*)H, k, wnorm2,
+                                                           (double2*)hcol, n);
+    LAUNCH_CHECK();
+    return RG_OK;
+}
+
+int rg_krylov_update(int dtype, int n, void* u, const void* Z, long long ldz, const void* y, int k,
+                     void* stream) {
+    if (!u || (k > 0 && (!Z || !y))) return fail(RG_ENULL, "null argument");
+    if (dtype != RG_F64 && dtype != RG_C128) return fail(RG_EINVAL, "update: float64 or complex128");
+    if (k <= 0) return RG_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    int nx = (n + MGS_NT * 2 - 1) / (MGS_NT * 2);
+    if (nx > 1184) nx = 1184;
+    if (dtype == RG_F64)
+        krylov_update_kernel<double><<<nx, MGS_NT, 0, st>>>((double*)u, (const double*)Z, ldz,
+                                                            (const double*)y, k, n);
+    else
+        krylov_update_kernel<double2><<<nx, MGS_NT, 0, st>>>((double2*)u, (const double2*)Z, ldz,
+                                                             (const double2*)y, k, n);
+    LAUNCH_CHECK();
+    return RG_OK;
 }
 
 int rg_solver_create(rg_solver** out, const rg_op* A, const rg_sched* s, double tol,

@@ -209,8 +209,11 @@ class GpuHierarchy:
             ud.zero_()
         return self._level(0, self._buf("f", 0), ud, pre, post)
 
-    def apply(self, f, u=None, pre=1, post=1):
+    def apply(self, f, u=None, pre=1, post=1, check=True):
         """One V-cycle on device tensors f, u [batch, P0]; returns a new tensor.
+        check=False skips the host-synchronising non-finite test of
+        multigrid.py:135-137 (callers that test later, e.g. the pipelined
+        FGMRES, which checks whenever a Hessenberg column is not finite).
 
         The ~200 launches of a cycle (smoother steps, residuals, transfers on
         7 levels) are captured once into a CUDA graph per (u given, pre,
@@ -239,7 +242,7 @@ class GpuHierarchy:
         else:
             out = self._cycle(u is None, pre, post)
         res = out.clone()
-        if not bool(torch.isfinite(res).all()):
+        if check and not bool(torch.isfinite(res).all()):
             m = self.levels[0].sched.m if self.levels[0].sched is not None else 0
             raise DivergenceError("smoother produced a non-finite iterate",
                                   inner_iteration=pre * m)
