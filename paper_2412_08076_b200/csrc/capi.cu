@@ -1170,6 +1170,7 @@ int rg_dst_create(rg_dst** out, int batch, int side) {
         (e = cudaMemcpy(D->tw, tw.data(), sizeof(double2) * M, cudaMemcpyHostToDevice)) != cudaSuccess) {
         cudaFree(D->tw);
         cudaFree(D->work);
+        cudaFree(D->work2);
         delete D;
         return fail(RG_ECUDA, "dst plan: %s", cudaGetErrorString(e));
     }
