@@ -14,6 +14,7 @@
 #include "../../include/richgpu.h"
 #include "block.cuh"
 #include "dst.cuh"
+#include "dstw.cuh"
 #include "mg.cuh"
 #include "cluster.cuh"
 #include "krylov.cuh"
@@ -342,6 +343,13 @@ struct rg_dst {
     int batch, side, M, logM, lpc;
     double2* tw;     // [M]
     double* work;    // [batch][side][side] residual / intermediate
+    // lean kernels (dstw.cu, M = 512 / 1024 / 2048): the intermediate lives in
+    // a padded [batch][M][M] array (entry (i, k) at i * M + k, row / column 0
+    // unused), so rows start 16-byte aligned and 4 adjacent columns of a row
+    // are one 32-byte sector
+    bool lean = false;
+    double* wpad = nullptr;
+    int num_sms = 148;
     // dense path (side + 1 not a power of two): the orthonormal DST-I matrix
     bool dense = false;
     double* S = nullptr;      // [side][side]
@@ -409,6 +417,35 @@ static int dst_pass(const rg_dst* D, int axis, int mode, const double* in, doubl
     else rc = axis == 0 ? go(dst_lines_kernel<0, 512, 0, 0>) : go(dst_lines_kernel<1, 512, 0, 0>);
     if (rc) return rc;
     LAUNCH_CHECK();
+    return RG_OK;
+}
+
+// Views of the lean kernels (dstw.cuh): unpadded [side][side] arrays and the
+// padded intermediate, walked by rows or by columns.
+static DstwView dstw_view(const double* p, int side, bool padded, bool by_cols) {
+    DstwView v;
+    const long long M = side + 1;
+    v.base = const_cast<double*>(p);
+    const long long rs = padded ? M : side;          // row stride
+    v.bs = rs * rs;
+    v.off = padded ? 0 : -(long long)(side + 1);     // (1, 1) is entry 0 of an unpadded array
+    v.ls = by_cols ? 1 : rs;
+    v.es = by_cols ? rs : 1;
+    return v;
+}
+
+static int dstw_pass(const rg_dst* D, bool col, int mode, const double* in, bool in_padded, double* out,
+                     bool out_padded, const double* lam, cudaStream_t st) {
+    DstwArgs a;
+    a.in = dstw_view(in, D->side, in_padded, col);
+    a.out = dstw_view(out, D->side, out_padded, col);
+    a.lam = dstw_view(lam, D->side, false, col);
+    a.tw = D->tw;
+    a.B = D->batch;
+    a.N = D->side;
+    a.s4 = -0.25 * sqrt(2.0 / D->M);
+    const cudaError_t e = launch_dstw(a, D->logM, col, mode, D->num_sms, st);
+    if (e != cudaSuccess) return fail(RG_ECUDA, "dst launch: %s", cudaGetErrorString(e));
     return RG_OK;
 }
 
@@ -1164,16 +1201,23 @@ int rg_dst_create(rg_dst** out, int batch, int side) {
         const double ang = M_PI * (double)k / (double)M;
         tw[k] = make_double2(cos(ang), sin(ang));
     }
+    D->lean = dstw_supported(M) && env_int("RG_DSTW", 1) != 0;
     cudaError_t e;
     if ((e = cudaMalloc((void**)&D->tw, sizeof(double2) * M)) != cudaSuccess ||
         (e = cudaMalloc((void**)&D->work, sizeof(double) * (size_t)batch * side * side)) != cudaSuccess ||
+        (D->lean && ((e = cudaMalloc((void**)&D->wpad, sizeof(double) * (size_t)batch * M * M)) != cudaSuccess ||
+                     (e = cudaMemset(D->wpad, 0, sizeof(double) * (size_t)batch * M * M)) != cudaSuccess)) ||
         (e = cudaMemcpy(D->tw, tw.data(), sizeof(double2) * M, cudaMemcpyHostToDevice)) != cudaSuccess) {
         cudaFree(D->tw);
         cudaFree(D->work);
         cudaFree(D->work2);
+        cudaFree(D->wpad);
         delete D;
         return fail(RG_ECUDA, "dst plan: %s", cudaGetErrorString(e));
     }
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&D->num_sms, cudaDevAttrMultiProcessorCount, dev);
     *out = D;
     return RG_OK;
 }
@@ -1184,6 +1228,7 @@ int rg_dst_destroy(rg_dst* D) {
     cudaFree(D->work);
     cudaFree(D->S);
     cudaFree(D->work2);
+    cudaFree(D->wpad);
     delete D;
     return RG_OK;
 }
@@ -1195,6 +1240,11 @@ int rg_dst2(const rg_dst* D, const double* in, double* out, void* stream) {
         int rc = dst_gemm(D, in, true, D->S, false, D->work2, GEMM_STORE, nullptr, st);
         if (rc) return rc;
         return dst_gemm(D, D->S, false, D->work2, true, out, GEMM_STORE, nullptr, st);
+    }
+    if (D->lean) {   // rows into the padded intermediate, columns out of it
+        int rc = dstw_pass(D, false, DSTW_PLAIN, in, false, D->wpad, true, nullptr, st);
+        if (rc) return rc;
+        return dstw_pass(D, true, DSTW_PLAIN, D->wpad, true, out, false, nullptr, st);
     }
     int rc = dst_pass(D, 0, DST_PLAIN, in, out, nullptr, st);
     if (rc) return rc;
@@ -1261,6 +1311,11 @@ int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u
         if ((rc = dst_gemm(D, D->S, false, D->work2, true, D->work, GEMM_LAM, lam, st))) return rc;
         if ((rc = dst_gemm(D, D->work, true, D->S, false, D->work2, GEMM_STORE, nullptr, st))) return rc;
         return dst_gemm(D, D->S, false, D->work2, true, u, GEMM_ADD, nullptr, st);
+    }
+    if (D->lean) {
+        if ((rc = dstw_pass(D, false, DSTW_PLAIN, D->work, false, D->wpad, true, nullptr, st))) return rc;
+        if ((rc = dstw_pass(D, true, DSTW_TWICE_LAM, D->wpad, true, D->wpad, true, lam, st))) return rc;
+        return dstw_pass(D, false, DSTW_ADD, D->wpad, true, u, false, nullptr, st);
     }
     if ((rc = dst_pass(D, 0, DST_PLAIN, D->work, D->work, nullptr, st))) return rc;
     if ((rc = dst_pass(D, 1, DST_TWICE_LAM, D->work, D->work, lam, st))) return rc;

@@ -402,7 +402,7 @@ struct GemmArgs {
     int N, mode;
 };
 
-__global__ void __launch_bounds__(GM_NT) dst_gemm_kernel(const GemmArgs a) {
+static __global__ void __launch_bounds__(GM_NT) dst_gemm_kernel(const GemmArgs a) {
     __shared__ double Ps[GM_K][GM_T + 1];   // P tile, transposed (k, row)
     __shared__ double Qs[GM_K][GM_T + 1];   // Q tile (k, col)
     const int N = a.N, b = blockIdx.z;
