@@ -11,22 +11,56 @@
 // (i, j-1), so the substitution is a slope-2 wavefront: point (i, j) can be
 // computed at step s = j + 2 i.
 //
-// One CTA per system.  Thread t owns grid row p0 + t of the current pass
-// (rows are processed in passes of blockDim.x), walks its row left to right
-// one point per step, and receives the row above through a warp shuffle
-// (lane - 1 computed x(i-1, j+1) in the previous step), through a two-slot
-// shared-memory mailbox across warps, and through `edge` (the last row of
-// the previous pass).  One __syncthreads per step.  The right-hand side is
-// prefetched PF points ahead.  Contributions are subtracted in the column
-// order of a column-oriented substitution and divided by the diagonal, as
-// the reference's triangular solves do; SuperLU stores the lower factor
-// pre-divided by the diagonal, so results agree to rounding (~1e-15), the
-// reference's own bar for these maps is 1e-13 (test_precond.py:33-62).
-// The backward (upper) solve is the same walk in reversed index order.
+// A thread-block cluster of up to 8 CTAs per system.  A pass covers
+// (CTAs x TRI_RPC) grid rows; compute thread t of CTA c owns row
+// p0 + c TRI_RPC + t and walks it left to right one point per step.  Inside
+// a warp the rows are skewed by two steps (lane l is at column sigma - 2 l
+// of the warp's local step sigma) and the row above arrives by warp
+// shuffle.  Warps are decoupled: global warp g runs TRI_D = 64 + TRI_PF
+// steps behind warp g - 1, TRI_PF more than the dependency needs, so what
+// lane 0 of a warp reads from the row above (the last row of the previous
+// warp) during a window of TRI_PF steps was produced before that window
+// began, and ONE __syncthreads per window (not per step) orders producer
+// and consumer.
+//
+// A lone warp issues in order, so every instruction between two steps of
+// the recurrence lengthens it (measured: the bare shuffle + select + 2 DFMA
+// step runs at 41 cycles, profiles/micro/fp64_chain.cu).  The compute warps
+// therefore do nothing but the recurrence: per window they load their rows'
+// TRI_PF right-hand sides and the TRI_PF look-ahead values of the row above
+// from shared memory, run TRI_PF steps in registers, and store the TRI_PF
+// unscaled results back over the right-hand sides.  Everything else belongs
+// to the mover warps (the second half of the CTA, one per compute warp):
+//   * cp.async of the right-hand sides a few windows ahead (8 lanes per row
+//     segment, coalesced) plus an L2 prefetch further ahead;
+//   * coalesced write-back of the previous window's results, with the output
+//     scale applied on the way;
+//   * the hand-off between CTAs: the mover of a CTA's last warp copies that
+//     warp's last row of the previous window into the boundary buffer of
+//     the next CTA (DSMEM, plain 8-byte stores over a sentinel), and the
+//     mover of the next CTA's first warp polls the columns of the coming
+//     window until they have landed.  No cluster barrier, flag or fence is
+//     on the path (a release store costs a MEMBAR.ALL.GPU that waits for
+//     the warp's outstanding global traffic), and a CTA only ever waits for
+//     its predecessor.
+// Inside a CTA the row above warp w is simply the staged last row of warp
+// w - 1 (windows k - 2 and k - 1, kept alive that long).
+//
+// A system's ~3.3 side dependent steps thus run on up to 8 SMs with 4
+// compute warps each; the single-CTA, barrier-per-step form took 0.80 ms
+// for SOR at 8 x 1023^2 (profiles/ncu_tri_r01.json).
+// Contributions are subtracted with FMAs from rhs/d; SuperLU stores the
+// lower factor pre-divided by the diagonal and substitutes column by
+// column, so results agree to rounding (~1e-15); the reference's own bar
+// for these maps is 1e-13 (test_precond.py:33-62).  The backward (upper)
+// solve is the same walk in reversed index order.
 #pragma once
+#include <cooperative_groups.h>
+#include <cstdio>
 #include "common.cuh"
 
 namespace rg {
+namespace cg = cooperative_groups;
 
 enum { TRI_SOR = 1, TRI_SSOR = 2, TRI_SOR_T = 3, TRI_SSOR_T = 4 };
 // Transposed maps (P.apply_transpose, precond.py:93-94,112-113; the training
@@ -34,11 +68,30 @@ enum { TRI_SOR = 1, TRI_SSOR = 2, TRI_SOR_T = 3, TRI_SSOR_T = 4 };
 // lower coefficients, so relax (D + wL)^{-T} r is the reverse-order sweep
 // with the lower coefficients, and (D + wU)^{-T} the forward sweep with the
 // upper ones.
-constexpr int TRI_PF = 8;
-// rows per pass (threads per CTA); a grid taller than this runs in passes
-#ifndef RG_TRI_NT_MAX
-#define RG_TRI_NT_MAX 1024
+#ifndef RG_TRI_DBG
+#define RG_TRI_DBG 0   // timing experiments only: 1 = no compute, 2 = no data movement
 #endif
+#ifndef RG_TRI_PF
+#define RG_TRI_PF 8
+#endif
+#ifndef RG_TRI_RPC
+#define RG_TRI_RPC 128
+#endif
+#ifndef RG_TRI_L2PF
+#define RG_TRI_L2PF 4                   // windows of L2 prefetch distance beyond the cp.async depth
+#endif
+#ifndef RG_TRI_NBUF
+#define RG_TRI_NBUF 8                   // staging buffers (power of two): cp.async runs NBUF - 3 windows ahead
+#endif
+constexpr int TRI_NBUF = RG_TRI_NBUF;
+constexpr int TRI_AHEAD = TRI_NBUF - 3; // a buffer is refilled two windows after its write-back
+constexpr int TRI_PF = RG_TRI_PF;       // steps per window (8 or 16)
+constexpr int TRI_WS = TRI_PF + 2;      // staged row stride: 16-byte aligned rows, conflict-free 128-bit access
+constexpr int TRI_D = 64 + TRI_PF;      // steps a warp lags its predecessor
+constexpr int TRI_RPC = RG_TRI_RPC;     // rows (compute threads) per CTA
+constexpr int TRI_NCW = TRI_RPC / 32;   // compute warps per CTA (+ as many movers)
+constexpr int TRI_MAXC = 8;             // CTAs per cluster (portable limit)
+static_assert(TRI_NBUF >= 4 && (TRI_NBUF & (TRI_NBUF - 1)) == 0, "staging depth");
 
 template <typename S>
 struct TriArgs {
@@ -49,149 +102,379 @@ struct TriArgs {
     const S* r;
     S* z;
     S* work;                // SSOR: forward result [B][P]
+    int nc;                 // CTAs per cluster
+};
+
+template <typename SI>
+__device__ __forceinline__ double tri_rhs(double slot) {
+    if (sizeof(SI) == 8) return slot;
+    return (double)__int_as_float(__double2loint(slot));   // f32 staged raw in the low word
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// Sentinel of the cross-CTA hand-off: a quiet NaN with a payload no
+// arithmetic produces.  The consumer CTA arms its boundary buffer with it,
+// the producer overwrites it with plain 8-byte DSMEM stores (single-copy
+// atomic), and the consumer re-reads a column until it is no longer the
+// sentinel.  Should an input carry this very NaN, the bounded spin accepts
+// it (the result is NaN either way).
+constexpr unsigned long long TRI_SENT = 0xFFF8B200DEAD0001ULL;
+constexpr int TRI_SPIN_MAX = 1 << 22;
+__device__ __forceinline__ double ld_volatile_shared(const double* p) {
+    double v;
+    asm volatile("ld.volatile.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)) : "memory");
+    return v;
+}
+__device__ __forceinline__ bool tri_is_sent(double v) {
+    return (unsigned long long)__double_as_longlong(v) == TRI_SENT;
+}
+__device__ __forceinline__ void tri_arm(double* bnd, int side) {
+    for (int i = threadIdx.x; i < side; i += blockDim.x) bnd[i] = __longlong_as_double((long long)TRI_SENT);
+}
+
+// boundary index of column col: shifted by one so that the TRI_PF look-ahead
+// columns of a window are 16-byte aligned
+__device__ __forceinline__ int tri_bnd_idx(int col, int side) { return col ? col - 1 : side - 1; }
+
+struct TriShared {
+    double* stage;   // [TRI_NBUF][TRI_RPC][TRI_WS]: right-hand sides, then unscaled results
+    double* bnd;     // [side]: the row above this CTA's first row (previous CTA / previous pass)
 };
 
 // One substitution sweep: dst = oscale * x where M x = rhs, M lower
 // triangular in traversal order (reversed index order when REV).
 // rhs = src, or d * src when MULD (SSOR's D * y).  Coefficients in
 // traversal order: l0 (i-1, j-1), l1 (i-1, j), l2 (i-1, j+1), l3 (i, j-1).
-//
-// Memory: at step s every thread touches a different grid row, so direct
-// loads/stores cost one L1 line per thread per step (measured ~340 ns per
-// wavefront step at 1023 rows).  Instead the steps run in windows of
-// TRI_PF: the rhs of window k+1 is fetched into shared memory with
-// cp.async while window k computes (each warp copies its own 32 rows, 8
-// lanes per row segment, coalesced), every step replaces its rhs slot with
-// the result, and the window is written back with coalesced stores.  The
-// step body itself touches only registers and shared memory.  Warps whose
-// rows have not started or are finished skip the compute (barriers only).
-// Arithmetic: x = rhs/d - (l0/d) nm1 - ... with FMAs (the kernel is
-// compiled without contraction; these are explicit): a different rounding
-// from SuperLU's, agreement ~1e-15, inside the reference's 1e-13 bar.
-constexpr int TRI_WS = TRI_PF + 1;   // padded row stride of the staging buffers
-
-
+// Windows in which all 32 lanes of a warp are inside the grid run
+// predicate-free.
 template <bool REV, bool MULD, bool SCALE, typename SI, typename SO>
-__device__ __forceinline__ void tri_sweep(const SI* __restrict__ src, SO* __restrict__ dst, int side,
-                                          int P, double oscale, double l0, double l1, double l2,
-                                          double l3, double d, double* edge, double (*xfer)[2],
-                                          double* stage) {
+__device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __restrict__ src,
+                                          SO* __restrict__ dst, int side, int P, double oscale,
+                                          double l0, double l1, double l2, double l3, double d,
+                                          const TriShared& sm, int nc) {
     static_assert(sizeof(SI) == 8 || sizeof(SI) == 4, "element size");
-    const int t = threadIdx.x, NT = blockDim.x, lane = t & 31, wp = t >> 5;
-    const int nw = NT >> 5;
+#if RG_TRI_DBG == 3
+    __shared__ long long tri_dbg[16][16];
+#endif
+    const int crank = (int)cl.block_rank();
+    const int lane = threadIdx.x & 31;
+    const bool mover = threadIdx.x >= TRI_RPC;
+    const int wp = (threadIdx.x >> 5) - (mover ? TRI_NCW : 0);   // compute warp (owned or served)
+    const int t = wp * 32 + lane;                                // row within the CTA
+    const int gw = crank * TRI_NCW + wp;                         // global warp of the pass
+    const int RPP = nc * TRI_RPC;                                // rows per pass
     const double rd = 1.0 / d;
-    l0 *= rd;
-    l1 *= rd;
-    l2 *= rd;
-    l3 *= rd;
-    // staging: [2][NT][TRI_WS] doubles (f32 inputs are staged as raw 4-byte
-    // words in the low half of each slot and widened on use)
-    for (int p0 = 0; p0 < side; p0 += NT) {
-        const int ip = p0 + t;
-        const bool row_ok = ip < side;
-        const int nrows = min(NT, side - p0);
-        const int nsteps = side + 2 * (nrows - 1);
+    const double m0 = -(l0 * rd), m1 = -(l1 * rd), m2 = -(l2 * rd), m3 = -(l3 * rd);
+    const int a0 = TRI_D * gw;              // lane 0 is at column s - a0 at step s
+    const int shift = a0 + 2 * lane;        // this row: column s - shift
+    // movers: element (row 32 wp + r8 + RPI it, slot) of window k is column
+    // c0 - 2 RPI it + TRI_PF k
+    constexpr int LPR = TRI_PF;              // lanes per row segment
+    constexpr int RPI = 32 / LPR;            // rows per copy instruction
+    constexpr int NIT = 32 / RPI;            // copy instructions per window
+    const int r8 = lane / LPR, slot = lane % LPR;
+    const int c0 = slot - a0 - 2 * r8;
+    const long long gstride = (long long)RPI * side - 2 * RPI;
+    const long long gs = REV ? -gstride : gstride;
+    const int dk = REV ? -TRI_PF : TRI_PF;
+    double* stage = sm.stage;
+    auto buf = [&](int k) { return stage + (size_t)(k & (TRI_NBUF - 1)) * TRI_RPC * TRI_WS; };
+    const bool cta_first = wp == 0, cta_last = wp == TRI_NCW - 1;
+    double* bnd_next = cl.map_shared_rank(sm.bnd, crank + 1 < nc ? crank + 1 : 0);
+    for (int p0 = 0; p0 < side; p0 += RPP) {
+        const int row = p0 + crank * TRI_RPC + t;                  // traversal-order grid row
+        const int wrow0 = row - lane;                              // first row of the warp
+        const bool row_ok = row < side;
+        const int nrows = min(RPP, side - p0);
+        const int last = nrows - 1;
+        const int nsteps = side + TRI_D * (last >> 5) + 2 * (last & 31);
         const int nwin = (nsteps + TRI_PF - 1) / TRI_PF;
-        const int a0 = 2 * 32 * wp;   // lane 0 starts at a0; lane 31 done at a0 + 62 + side
-        if (t < nw) xfer[t][0] = xfer[t][1] = 0.0;
-        auto gidx = [&](int row, int c) -> long long {   // row: index within the pass
-            const long long g = (long long)(p0 + row) * side + c;
-            return REV ? (long long)P - 1 - g : g;
-        };
+        // the warp's last row goes to the next CTA, or (last CTA) to CTA 0 for the next pass
+        const bool pushes = cta_last && wrow0 + 31 < side &&
+                            (crank + 1 < nc ? wrow0 + 32 < side : p0 + RPP < side);
+        const bool polls = cta_first && crank > 0;                 // row above comes from the previous CTA
+        const bool has_above = wp > 0 || crank > 0 || p0 > 0;
+        const long long g0 = (long long)(wrow0 + r8) * side + c0;
+        const SI* sp = src + (REV ? (long long)P - 1 - g0 : g0);
+        SO* dp = dst + (REV ? (long long)P - 1 - g0 : g0);
+        // window k of this warp: idle (nothing of the warp inside the grid,
+        // not even lane 0's warm-up step), or interior (every lane inside
+        // for all TRI_PF steps, and lane 0's look-ahead column too)
         auto idle_win = [&](int k) {
-            const int s0 = k * TRI_PF;
-            return (s0 + TRI_PF <= a0 - 1) || (s0 > a0 + 62 + side);
+            const int s0 = k * TRI_PF - a0;
+            return k < 0 || k >= nwin || wrow0 >= side || s0 + TRI_PF <= -1 || s0 > 62 + side - 1;
         };
-        // warp-cooperative window copies: lane -> (row 32 wp + lane/8 + 4 it, slot lane%8)
-        auto load_win = [&](int k) {
-            double* b = stage + (size_t)(k & 1) * NT * TRI_WS;
-#pragma unroll
-            for (int it = 0; it < 8; ++it) {
-                const int row = wp * 32 + (lane >> 3) + 4 * it;
-                const int c = k * TRI_PF + (lane & 7) - 2 * row;
-                const bool ok = p0 + row < side && c >= 0 && c < side;
-                cp_async_el<sizeof(SI)>(&b[row * TRI_WS + (lane & 7)], src + (ok ? gidx(row, c) : 0), ok);
-            }
-            cp_async_commit();
+        auto interior = [&](int k) {
+            const int s0 = k * TRI_PF - a0;
+            return wrow0 + 31 < side && s0 >= 62 && s0 + TRI_PF <= side - 1;
         };
-        auto store_win = [&](int k) {
-            const double* b = stage + (size_t)(k & 1) * NT * TRI_WS;
+        auto load_win = [&](int k) {     // rhs of window k -> its staging buffer
+            double* b = buf(k) + (size_t)(wp * 32 + r8) * TRI_WS + slot;
+            const SI* s = sp + (long long)k * dk;
+            if (interior(k)) {
 #pragma unroll
-            for (int it = 0; it < 8; ++it) {
-                const int row = wp * 32 + (lane >> 3) + 4 * it;
-                const int c = k * TRI_PF + (lane & 7) - 2 * row;
-                if (p0 + row < side && c >= 0 && c < side)
-                    dst[gidx(row, c)] = (SO)b[row * TRI_WS + (lane & 7)];
+                for (int it = 0; it < NIT; ++it)
+                    cp_async_el<sizeof(SI)>(b + it * RPI * TRI_WS, s + it * gs, true);
+            } else {
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) {
+                    const int c = c0 - 2 * RPI * it + k * TRI_PF;
+                    const bool ok = wrow0 + r8 + RPI * it < side && (unsigned)c < (unsigned)side;
+                    cp_async_el<sizeof(SI)>(b + it * RPI * TRI_WS, ok ? s + it * gs : src, ok);
+                }
             }
         };
-        auto rhs_at = [&](const double* slot) -> double {
-            if (sizeof(SI) == 8) return *slot;
-            return (double)*reinterpret_cast<const float*>(slot);
+        auto store_win = [&](int k) {    // results of window k -> dst
+            const double* b = buf(k) + (size_t)(wp * 32 + r8) * TRI_WS + slot;
+            SO* o = dp + (long long)k * dk;
+            if (interior(k)) {
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) {
+                    const double x = b[it * RPI * TRI_WS];
+                    o[it * gs] = (SO)(SCALE ? oscale * x : x);
+                }
+            } else {
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) {
+                    const int c = c0 - 2 * RPI * it + k * TRI_PF;
+                    if (wrow0 + r8 + RPI * it < side && (unsigned)c < (unsigned)side) {
+                        const double x = b[it * RPI * TRI_WS];
+                        o[it * gs] = (SO)(SCALE ? oscale * x : x);
+                    }
+                }
+            }
         };
-        if (!idle_win(0)) load_win(0);
-        double left = 0.0, nm1 = 0.0, n0 = 0.0, pub = 0.0;
-        // thread 0 starts at column 0 with no warm-up steps: x(i-1, 0) of the
-        // previous pass's last row seeds its window (zero for the first pass)
-        if (t == 0 && p0 > 0) n0 = edge[0];
-        for (int k = 0; k < nwin; ++k) {
-            const bool idle = idle_win(k);
-            cp_async_wait_all();          // window k's rhs (issued one window ago)
+        auto prefetch_win = [&](int k) { // one lane per row: window k's segment -> L2
+            int c = k * TRI_PF - shift;
+            if (!row_ok || c + TRI_PF <= 0 || c >= side) return;
+            c = max(c, 0);
+            const long long g = (long long)row * side + c;
+            prefetch_l2(src + (REV ? (long long)P - 1 - g : g));
+        };
+        auto push_win = [&](int k) {     // last row of window k -> the next CTA's boundary buffer
+            if (lane < TRI_PF) {
+                const int col = k * TRI_PF + lane - a0 - 62;
+                if ((unsigned)col < (unsigned)side)
+                    bnd_next[tri_bnd_idx(col, side)] = buf(k)[(size_t)(wp * 32 + 31) * TRI_WS + lane];
+            }
+        };
+        auto poll_win = [&](int k) {     // look-ahead columns of window k have landed
+            if (lane < TRI_PF) {
+                const int col = k * TRI_PF + lane - a0 + 1;
+                if ((unsigned)col < (unsigned)side) {
+                    const double* q = sm.bnd + tri_bnd_idx(col, side);
+                    for (int spin = 0; spin < TRI_SPIN_MAX; ++spin)
+                        if (!tri_is_sent(ld_volatile_shared(q))) break;
+                }
+            }
             __syncwarp();
-            if (k + 1 < nwin && !idle_win(k + 1)) load_win(k + 1);
-            __syncthreads();
-            if (idle) {
-#pragma unroll
-                for (int q = 0; q < TRI_PF - 1; ++q) __syncthreads();
+        };
+        double left = 0.0, nm1 = 0.0, n0 = 0.0, pub = 0.0;
+        if (mover) {
+            for (int k = 0; k < TRI_AHEAD; ++k) {
+                if (!idle_win(k)) load_win(k);
+                cp_async_commit();
+            }
+            if (polls && !idle_win(0)) poll_win(0);
+        } else if (t == 0 && crank == 0 && p0 > 0) {
+            // the pass's first row starts at column 0 with no warm-up step:
+            // x(i-1, 0) of the previous pass's last row seeds its window
+            n0 = sm.bnd[tri_bnd_idx(0, side)];
+        }
+        // window k: [barrier] the movers hand on and write back window k-1
+        // and fetch window k + AHEAD (into the buffer window k-3 left) while
+        // the owners compute window k; one extra round drains
+        for (int k = 0; k <= nwin; ++k) {
+            if (mover) cp_async_wait_group<TRI_AHEAD - 1>();   // window k's rhs has landed
+            __syncthreads();                                   // + results of window k-1 visible
+            if (mover) {
+#if RG_TRI_DBG == 2
+                continue;
+#endif
+#if RG_TRI_DBG == 3
+                if (blockIdx.x == 0 && lane == 0 && k >= 60 && k < 76) tri_dbg[k - 60][8 + 2 * wp] = clock64();
+#endif
+                if (!idle_win(k - 1)) {
+                    if (pushes) push_win(k - 1);
+                    store_win(k - 1);
+                }
+                if (!idle_win(k + TRI_AHEAD)) load_win(k + TRI_AHEAD);
+                cp_async_commit();
+                if (RG_TRI_L2PF > 0) prefetch_win(k + TRI_AHEAD + RG_TRI_L2PF);
+                if (polls && !idle_win(k + 1)) poll_win(k + 1);
+#if RG_TRI_DBG == 3
+                if (blockIdx.x == 0 && lane == 0 && k >= 60 && k < 76) tri_dbg[k - 60][9 + 2 * wp] = clock64();
+#endif
                 continue;
             }
-            double* b = stage + ((size_t)(k & 1) * NT + t) * TRI_WS;
+#if RG_TRI_DBG == 1
+            continue;
+#endif
+            if (idle_win(k)) continue;
+#if RG_TRI_DBG == 3
+            long long tk0 = clock64(), tk1 = 0, tk2 = 0;
+#endif
             const int s0 = k * TRI_PF;
+            double2* b2 = reinterpret_cast<double2*>(buf(k) + (size_t)t * TRI_WS);
+            double raw[TRI_PF], rb[TRI_PF];
 #pragma unroll
-            for (int q = 0; q < TRI_PF; ++q) {
-                const int s = s0 + q;
-                const int jp = s - 2 * t;
-                const bool act = row_ok && (unsigned)jp < (unsigned)side;
-                // x(i-1, j+1): lane - 1 (shuffle), the previous warp's lane 31
-                // (mailbox) or the previous pass's last row (edge); selects
-                // instead of a divergent branch
-                const double sh = __shfl_up_sync(0xffffffffu, pub, 1);
-                const double mb = xfer[wp][(s + 1) & 1];
-                const int ce = min(max(jp + 1, 0), side - 1);
-                const double ev = (p0 > 0 && (unsigned)(jp + 1) < (unsigned)side) ? edge[ce] : 0.0;
-                const double nb = lane != 0 ? sh : (wp > 0 ? mb : ev);
-                // x = (rhs - l0 nm1 - l1 n0 - l2 nb - l3 left) / d, as
-                // rhs/d - (l/d) x with FMAs: two dependent FMAs per step
-                // after the neighbour value arrives
-                const double rv = rhs_at(&b[q]);
-                double u = MULD ? rv : rv * rd;          // (d y) / d = y for SSOR's D y
-                u = __fma_rn(-l0, nm1, u);
-                u = __fma_rn(-l1, n0, u);
-                u = __fma_rn(-l2, nb, u);
-                const double x = act ? __fma_rn(-l3, left, u) : 0.0;
-                b[q] = SCALE ? oscale * x : x;
-                if (act && t == NT - 1) edge[jp] = x;
-                nm1 = n0;
-                n0 = nb;
-                left = x;
-                pub = x;
-                if (lane == 31 && wp + 1 < nw) xfer[wp + 1][s & 1] = x;
-                if (q + 1 < TRI_PF) __syncthreads();
+            for (int q = 0; q < TRI_PF; q += 2) {
+                const double2 v = b2[q >> 1];
+                raw[q] = v.x;
+                raw[q + 1] = v.y;
             }
-            __syncwarp();
-            store_win(k);
+#if RG_TRI_DBG == 3
+            tk1 = clock64();
+#endif
+            if (interior(k)) {
+                // x(i-1, j+1) for lane 0 over the window: columns
+                // s0 - a0 + 1 + q of the row above
+                if (wp > 0) {
+                    // previous warp's last row: its lane 31 computed column
+                    // s0 - a0 + 1 + q at step s0 + q - 1 - TRI_PF, i.e. the last
+                    // slot of window k - 2 for q = 0, slot q - 1 of window k - 1
+                    // after that
+                    const double* pr2 = buf(k - 2) + (size_t)(wp * 32 - 1) * TRI_WS;
+                    const double* pr1 = buf(k - 1) + (size_t)(wp * 32 - 1) * TRI_WS;
+                    rb[0] = pr2[TRI_PF - 1];
+#pragma unroll
+                    for (int q = 1; q + 1 < TRI_PF; q += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(pr1 + q - 1);
+                        rb[q] = v.x;
+                        rb[q + 1] = v.y;
+                    }
+                    rb[TRI_PF - 1] = pr1[TRI_PF - 2];
+                } else if (has_above) {
+                    const double2* r2 = reinterpret_cast<const double2*>(sm.bnd + (s0 - a0));
+#pragma unroll
+                    for (int q = 0; q < TRI_PF; q += 2) {
+                        const double2 v = r2[q >> 1];
+                        rb[q] = v.x;
+                        rb[q + 1] = v.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < TRI_PF; ++q) rb[q] = 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < TRI_PF; ++q) {
+#if RG_TRI_DBG == 4
+                    const double nb = lane != 0 ? pub : rb[q];
+#else
+                    const double sh = __shfl_up_sync(0xffffffffu, pub, 1);
+                    const double nb = lane != 0 ? sh : rb[q];
+#endif
+                    const double rv = tri_rhs<SI>(raw[q]);
+#if RG_TRI_DBG == 5
+                    const double x = __longlong_as_double(__double_as_longlong(nb) ^ __double_as_longlong(rv) ^ __double_as_longlong(left));
+#else
+                    double u = MULD ? rv : rv * rd;          // (d y) / d = y for SSOR's D y
+                    u = __fma_rn(m0, nm1, u);
+                    u = __fma_rn(m1, n0, u);
+                    u = __fma_rn(m3, left, u);
+                    const double x = __fma_rn(m2, nb, u);   // the value that arrives last goes last
+#endif
+                    raw[q] = x;
+                    nm1 = n0;
+                    n0 = nb;
+                    left = x;
+                    pub = x;
+                }
+            } else {
+                if (wp > 0) {
+                    // same slots as above; columns outside the grid were not
+                    // computed by the row above (stale slots): masked to zero
+                    const double* pr2 = buf(k - 2) + (size_t)(wp * 32 - 1) * TRI_WS;
+                    const double* pr1 = buf(k - 1) + (size_t)(wp * 32 - 1) * TRI_WS;
+                    rb[0] = pr2[TRI_PF - 1];
+#pragma unroll
+                    for (int q = 1; q + 1 < TRI_PF; q += 2) {
+                        const double2 v = *reinterpret_cast<const double2*>(pr1 + q - 1);
+                        rb[q] = v.x;
+                        rb[q + 1] = v.y;
+                    }
+                    rb[TRI_PF - 1] = pr1[TRI_PF - 2];
+#pragma unroll
+                    for (int q = 0; q < TRI_PF; ++q)
+                        if ((unsigned)(s0 + q - a0 + 1) >= (unsigned)side) rb[q] = 0.0;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < TRI_PF; ++q) {
+                        const int col = s0 + q - a0 + 1;
+                        rb[q] = 0.0;
+                        if (has_above && (unsigned)col < (unsigned)side) rb[q] = sm.bnd[tri_bnd_idx(col, side)];
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < TRI_PF; ++q) {
+                    const int jp = s0 + q - shift;
+                    const bool act = row_ok && (unsigned)jp < (unsigned)side;
+                    const double sh = __shfl_up_sync(0xffffffffu, pub, 1);
+                    const double nb = lane != 0 ? sh : rb[q];
+                    const double rv = tri_rhs<SI>(raw[q]);
+                    double u = MULD ? rv : rv * rd;
+                    u = __fma_rn(m0, nm1, u);
+                    u = __fma_rn(m1, n0, u);
+                    u = __fma_rn(m3, left, u);
+                    const double x = act ? __fma_rn(m2, nb, u) : 0.0;
+                    raw[q] = x;
+                    nm1 = n0;
+                    n0 = nb;
+                    left = x;
+                    pub = x;
+                }
+            }
+#if RG_TRI_DBG == 3
+            tk2 = clock64();
+#endif
+#pragma unroll
+            for (int q = 0; q < TRI_PF; q += 2) b2[q >> 1] = make_double2(raw[q], raw[q + 1]);
+#if RG_TRI_DBG == 3
+            if (blockIdx.x == 0 && lane == 0 && k >= 60 && k < 76) {
+                tri_dbg[k - 60][2 * wp] = tk0;
+                tri_dbg[k - 60][2 * wp + 1] = clock64();
+            }
+#endif
         }
-        cp_async_wait_all();
+#if RG_TRI_DBG == 3
         __syncthreads();
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            for (int i = 0; i < 16; ++i) {
+                const long long z = tri_dbg[0][0];
+                printf("k %d:", 60 + i);
+                for (int w = 0; w < 8; ++w) printf(" [%lld %lld]", tri_dbg[i][2 * w] - z, tri_dbg[i][2 * w + 1] - tri_dbg[i][2 * w]);
+                printf("\n");
+            }
+#endif
+        if (mover) cp_async_wait_all();
+        // passes and sweeps: boundary rows handed to CTA 0 and global results
+        // must be complete before anyone starts the next one, and the
+        // boundary buffers of CTAs >= 1 (fully consumed by now) are armed
+        // again before their producers restart
+        if (nc > 1) {
+            __syncthreads();
+            if (crank > 0) tri_arm(sm.bnd, side);
+            cl.sync();
+        } else {
+            __syncthreads();
+        }
     }
 }
 
 template <typename S, int MODE>
-__global__ void __launch_bounds__(1024, 1) tri_kernel(const TriArgs<S> a) {
+__global__ void __launch_bounds__(2 * TRI_RPC, 1) tri_kernel(const TriArgs<S> a) {
     extern __shared__ double tri_smem[];
-    double* stage = tri_smem;                                        // [2][NT][TRI_WS]
-    double* edge = tri_smem + 2 * (size_t)blockDim.x * TRI_WS;        // [side]
-    __shared__ double xfer[32][2];
-    const int b = blockIdx.x;
+    cg::cluster_group cl = cg::this_cluster();
+    TriShared sm;
+    sm.stage = tri_smem;                                          // [TRI_NBUF][TRI_RPC][TRI_WS]
+    sm.bnd = sm.stage + (size_t)TRI_NBUF * TRI_RPC * TRI_WS;      // [side + 1]
+    if (a.nc > 1) {
+        if (cl.block_rank() > 0) tri_arm(sm.bnd, a.side);
+        cl.sync();                                                // armed before any producer store lands
+    }
+    const int b = blockIdx.x / a.nc;
     const double* c = a.stencil + (size_t)(a.shared ? 0 : b) * 9;
     const double w = a.relax;
     // DL = diag + relax * tril(A, -1), DU = diag + relax * triu(A, 1) (precond.py:91,104-105)
@@ -201,43 +484,50 @@ __global__ void __launch_bounds__(1024, 1) tri_kernel(const TriArgs<S> a) {
     const size_t base = (size_t)b * a.P;
     if (MODE == TRI_SOR) {
         // relax * solve(r)  (precond.py:93)
-        tri_sweep<false, false, true, S, S>(a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
-                                            lo3, d, edge, xfer, stage);
+        tri_sweep<false, false, true, S, S>(cl, a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
+                                            lo3, d, sm, a.nc);
     } else if (MODE == TRI_SOR_T) {
         // relax * solve_t(r)  (precond.py:94)
-        tri_sweep<true, false, true, S, S>(a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
-                                           lo3, d, edge, xfer, stage);
+        tri_sweep<true, false, true, S, S>(cl, a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
+                                           lo3, d, sm, a.nc);
     } else if (MODE == TRI_SSOR_T) {
         // c * dlt(diag * dut(r))  (precond.py:112-113)
         const double cc = w * (2.0 - w);
-        tri_sweep<false, false, false, S, S>(a.r + base, a.work + base, a.side, a.P, 1.0, up0, up1,
-                                             up2, up3, d, edge, xfer, stage);
-        __syncthreads();
-        tri_sweep<true, true, true, S, S>(a.work + base, a.z + base, a.side, a.P, cc, lo0, lo1, lo2,
-                                          lo3, d, edge, xfer, stage);
+        tri_sweep<false, false, false, S, S>(cl, a.r + base, a.work + base, a.side, a.P, 1.0, up0, up1,
+                                             up2, up3, d, sm, a.nc);
+        tri_sweep<true, true, true, S, S>(cl, a.work + base, a.z + base, a.side, a.P, cc, lo0, lo1, lo2,
+                                          lo3, d, sm, a.nc);
     } else {
         // c * du(diag * dl(r))  (precond.py:109-110)
         const double cc = w * (2.0 - w);
-        tri_sweep<false, false, false, S, S>(a.r + base, a.work + base, a.side, a.P, 1.0, lo0, lo1,
-                                             lo2, lo3, d, edge, xfer, stage);
-        __syncthreads();
-        tri_sweep<true, true, true, S, S>(a.work + base, a.z + base, a.side, a.P, cc, up0, up1, up2,
-                                          up3, d, edge, xfer, stage);
+        tri_sweep<false, false, false, S, S>(cl, a.r + base, a.work + base, a.side, a.P, 1.0, lo0, lo1,
+                                             lo2, lo3, d, sm, a.nc);
+        tri_sweep<true, true, true, S, S>(cl, a.work + base, a.z + base, a.side, a.P, cc, up0, up1, up2,
+                                          up3, d, sm, a.nc);
     }
 }
 
 template <typename S, int MODE>
-cudaError_t launch_tri_m(const TriArgs<S>& a, int batch, cudaStream_t st) {
-    int nt = (a.side + 31) / 32 * 32;
-    if (nt > RG_TRI_NT_MAX) nt = RG_TRI_NT_MAX;
-    const size_t smem = (2 * (size_t)nt * TRI_WS + a.side) * sizeof(double);
+cudaError_t launch_tri_m(TriArgs<S> a, int batch, cudaStream_t st) {
+    a.nc = (a.side + TRI_RPC - 1) / TRI_RPC;
+    if (a.nc > TRI_MAXC) a.nc = TRI_MAXC;
+    const size_t smem = ((size_t)TRI_NBUF * TRI_RPC * TRI_WS + a.side + 1) * sizeof(double);
     auto k = tri_kernel<S, MODE>;
-    {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    k<<<batch, nt, smem, st>>>(a);
-    return cudaGetLastError();
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(batch * a.nc, 1, 1);
+    cfg.blockDim = dim3(2 * TRI_RPC, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.nc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, a);
 }
 
 template <typename S>

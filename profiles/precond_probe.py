@@ -34,6 +34,7 @@ def ev_time(fn, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="application timings only")
     args = ap.parse_args()
     out = {}
     rng = np.random.default_rng(0)
@@ -60,6 +61,10 @@ def main():
                 f(r0)
             row["cpu_ssor_ms_per_system"] = (time.perf_counter() - t0) / 3 * 1e3
         out[f"{n - 1}^2 x {B}"] = row
+    if args.quick:
+        print(json.dumps({k: {m: round(v[m]["ms_per_apply_batch"], 4) for m in ("sor", "ssor")}
+                          for k, v in out.items()}))
+        return
     # NAG(3) + SSOR solve to 1e-6 at 1023^2 x 8 (weights for B^{-1}A in (0, 1])
     n, B = 1024, 8
     As = [O.assemble_anisotropic(10 ** rng.uniform(-2, 0), rng.uniform(0, np.pi), n)
