@@ -56,7 +56,6 @@
 // solve is the same walk in reversed index order.
 #pragma once
 #include <cooperative_groups.h>
-#include <cstdio>
 #include "common.cuh"
 
 namespace rg {
@@ -68,17 +67,17 @@ enum { TRI_SOR = 1, TRI_SSOR = 2, TRI_SOR_T = 3, TRI_SSOR_T = 4 };
 // lower coefficients, so relax (D + wL)^{-T} r is the reverse-order sweep
 // with the lower coefficients, and (D + wU)^{-T} the forward sweep with the
 // upper ones.
-#ifndef RG_TRI_DBG
-#define RG_TRI_DBG 0   // timing experiments only: 1 = no compute, 2 = no data movement
+#ifndef RG_TRI_SKIP
+#define RG_TRI_SKIP 0  // timing experiments only: bit 0 no fetch, bit 1 no write-back, bit 2 no CTA hand-off, bit 3 no compute
 #endif
 #ifndef RG_TRI_PF
-#define RG_TRI_PF 8
+#define RG_TRI_PF 16
 #endif
 #ifndef RG_TRI_RPC
 #define RG_TRI_RPC 128
 #endif
 #ifndef RG_TRI_L2PF
-#define RG_TRI_L2PF 4                   // windows of L2 prefetch distance beyond the cp.async depth
+#define RG_TRI_L2PF 0                   // windows of L2 prefetch distance beyond the cp.async depth (0: none; measured no gain)
 #endif
 #ifndef RG_TRI_NBUF
 #define RG_TRI_NBUF 8                   // staging buffers (power of two): cp.async runs NBUF - 3 windows ahead
@@ -155,13 +154,11 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
                                           double l0, double l1, double l2, double l3, double d,
                                           const TriShared& sm, int nc) {
     static_assert(sizeof(SI) == 8 || sizeof(SI) == 4, "element size");
-#if RG_TRI_DBG == 3
-    __shared__ long long tri_dbg[16][16];
-#endif
     const int crank = (int)cl.block_rank();
     const int lane = threadIdx.x & 31;
-    const bool mover = threadIdx.x >= TRI_RPC;
-    const int wp = (threadIdx.x >> 5) - (mover ? TRI_NCW : 0);   // compute warp (owned or served)
+    const int role = threadIdx.x / TRI_RPC;                      // 0 compute, 1 write-back, 2 fetch
+    const bool mover = role > 0, storer = role == 1, loader = role == 2;
+    const int wp = (threadIdx.x >> 5) - role * TRI_NCW;          // compute warp (owned or served)
     const int t = wp * 32 + lane;                                // row within the CTA
     const int gw = crank * TRI_NCW + wp;                         // global warp of the pass
     const int RPP = nc * TRI_RPC;                                // rows per pass
@@ -202,14 +199,18 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
         // window k of this warp: idle (nothing of the warp inside the grid,
         // not even lane 0's warm-up step), or interior (every lane inside
         // for all TRI_PF steps, and lane 0's look-ahead column too)
-        auto idle_win = [&](int k) {
-            const int s0 = k * TRI_PF - a0;
-            return k < 0 || k >= nwin || wrow0 >= side || s0 + TRI_PF <= -1 || s0 > 62 + side - 1;
-        };
-        auto interior = [&](int k) {
-            const int s0 = k * TRI_PF - a0;
-            return wrow0 + 31 < side && s0 >= 62 && s0 + TRI_PF <= side - 1;
-        };
+        // (as window ranges, so that the per-window tests are two compares:
+        //  idle: s0 + PF <= -1 or s0 > 62 + side - 1 with s0 = k PF - a0;
+        //  interior: s0 >= 62 and s0 + PF <= side - 1, all 32 rows inside)
+        int k_first = max(0, (a0 - TRI_PF) / TRI_PF);
+        while (k_first * TRI_PF - a0 + TRI_PF <= -1) ++k_first;
+        int k_last = min(nwin - 1, (a0 + 61 + side) / TRI_PF);
+        if (wrow0 >= side) k_last = -1;
+        int i_first = (a0 + 62 + TRI_PF - 1) / TRI_PF;
+        int i_last = (a0 + side - 1 - TRI_PF) / TRI_PF;
+        if (wrow0 + 31 >= side || a0 + side - 1 - TRI_PF < 0) i_last = -1;
+        auto idle_win = [&](int k) { return k < k_first || k > k_last; };
+        auto interior = [&](int k) { return k >= i_first && k <= i_last; };
         auto load_win = [&](int k) {     // rhs of window k -> its staging buffer
             double* b = buf(k) + (size_t)(wp * 32 + r8) * TRI_WS + slot;
             const SI* s = sp + (long long)k * dk;
@@ -230,11 +231,11 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
             const double* b = buf(k) + (size_t)(wp * 32 + r8) * TRI_WS + slot;
             SO* o = dp + (long long)k * dk;
             if (interior(k)) {
+                double x[NIT];
 #pragma unroll
-                for (int it = 0; it < NIT; ++it) {
-                    const double x = b[it * RPI * TRI_WS];
-                    o[it * gs] = (SO)(SCALE ? oscale * x : x);
-                }
+                for (int it = 0; it < NIT; ++it) x[it] = b[it * RPI * TRI_WS];
+#pragma unroll
+                for (int it = 0; it < NIT; ++it) o[it * gs] = (SO)(SCALE ? oscale * x[it] : x[it]);
             } else {
 #pragma unroll
                 for (int it = 0; it < NIT; ++it) {
@@ -259,6 +260,7 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
                 if ((unsigned)col < (unsigned)side)
                     bnd_next[tri_bnd_idx(col, side)] = buf(k)[(size_t)(wp * 32 + 31) * TRI_WS + lane];
             }
+
         };
         auto poll_win = [&](int k) {     // look-ahead columns of window k have landed
             if (lane < TRI_PF) {
@@ -272,12 +274,13 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
             __syncwarp();
         };
         double left = 0.0, nm1 = 0.0, n0 = 0.0, pub = 0.0;
-        if (mover) {
+        if (loader) {
             for (int k = 0; k < TRI_AHEAD; ++k) {
                 if (!idle_win(k)) load_win(k);
                 cp_async_commit();
             }
             if (polls && !idle_win(0)) poll_win(0);
+        } else if (storer) {
         } else if (t == 0 && crank == 0 && p0 > 0) {
             // the pass's first row starts at column 0 with no warm-up step:
             // x(i-1, 0) of the previous pass's last row seeds its window
@@ -287,35 +290,25 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
         // and fetch window k + AHEAD (into the buffer window k-3 left) while
         // the owners compute window k; one extra round drains
         for (int k = 0; k <= nwin; ++k) {
-            if (mover) cp_async_wait_group<TRI_AHEAD - 1>();   // window k's rhs has landed
+            if (loader) cp_async_wait_group<TRI_AHEAD - 1>();  // window k's rhs has landed
             __syncthreads();                                   // + results of window k-1 visible
             if (mover) {
-#if RG_TRI_DBG == 2
-                continue;
-#endif
-#if RG_TRI_DBG == 3
-                if (blockIdx.x == 0 && lane == 0 && k >= 60 && k < 76) tri_dbg[k - 60][8 + 2 * wp] = clock64();
-#endif
-                if (!idle_win(k - 1)) {
-                    if (pushes) push_win(k - 1);
-                    store_win(k - 1);
+                if ((RG_TRI_SKIP & 1) && loader) continue;
+                if (storer) {
+                    if (!idle_win(k - 1)) {
+                        if (pushes && !(RG_TRI_SKIP & 4)) push_win(k - 1);
+                        if (!(RG_TRI_SKIP & 2)) store_win(k - 1);
+                    }
+                } else {
+                    if (!idle_win(k + TRI_AHEAD)) load_win(k + TRI_AHEAD);
+                    cp_async_commit();
+                    if (RG_TRI_L2PF > 0) prefetch_win(k + TRI_AHEAD + RG_TRI_L2PF);
+                    if (polls && !idle_win(k + 1) && !(RG_TRI_SKIP & 4)) poll_win(k + 1);
                 }
-                if (!idle_win(k + TRI_AHEAD)) load_win(k + TRI_AHEAD);
-                cp_async_commit();
-                if (RG_TRI_L2PF > 0) prefetch_win(k + TRI_AHEAD + RG_TRI_L2PF);
-                if (polls && !idle_win(k + 1)) poll_win(k + 1);
-#if RG_TRI_DBG == 3
-                if (blockIdx.x == 0 && lane == 0 && k >= 60 && k < 76) tri_dbg[k - 60][9 + 2 * wp] = clock64();
-#endif
                 continue;
             }
-#if RG_TRI_DBG == 1
-            continue;
-#endif
+            if (RG_TRI_SKIP & 8) continue;
             if (idle_win(k)) continue;
-#if RG_TRI_DBG == 3
-            long long tk0 = clock64(), tk1 = 0, tk2 = 0;
-#endif
             const int s0 = k * TRI_PF;
             double2* b2 = reinterpret_cast<double2*>(buf(k) + (size_t)t * TRI_WS);
             double raw[TRI_PF], rb[TRI_PF];
@@ -325,9 +318,6 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
                 raw[q] = v.x;
                 raw[q + 1] = v.y;
             }
-#if RG_TRI_DBG == 3
-            tk1 = clock64();
-#endif
             if (interior(k)) {
                 // x(i-1, j+1) for lane 0 over the window: columns
                 // s0 - a0 + 1 + q of the row above
@@ -360,22 +350,14 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
                 }
 #pragma unroll
                 for (int q = 0; q < TRI_PF; ++q) {
-#if RG_TRI_DBG == 4
-                    const double nb = lane != 0 ? pub : rb[q];
-#else
                     const double sh = __shfl_up_sync(0xffffffffu, pub, 1);
                     const double nb = lane != 0 ? sh : rb[q];
-#endif
                     const double rv = tri_rhs<SI>(raw[q]);
-#if RG_TRI_DBG == 5
-                    const double x = __longlong_as_double(__double_as_longlong(nb) ^ __double_as_longlong(rv) ^ __double_as_longlong(left));
-#else
                     double u = MULD ? rv : rv * rd;          // (d y) / d = y for SSOR's D y
                     u = __fma_rn(m0, nm1, u);
                     u = __fma_rn(m1, n0, u);
                     u = __fma_rn(m3, left, u);
                     const double x = __fma_rn(m2, nb, u);   // the value that arrives last goes last
-#endif
                     raw[q] = x;
                     nm1 = n0;
                     n0 = nb;
@@ -426,29 +408,10 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
                     pub = x;
                 }
             }
-#if RG_TRI_DBG == 3
-            tk2 = clock64();
-#endif
 #pragma unroll
             for (int q = 0; q < TRI_PF; q += 2) b2[q >> 1] = make_double2(raw[q], raw[q + 1]);
-#if RG_TRI_DBG == 3
-            if (blockIdx.x == 0 && lane == 0 && k >= 60 && k < 76) {
-                tri_dbg[k - 60][2 * wp] = tk0;
-                tri_dbg[k - 60][2 * wp + 1] = clock64();
-            }
-#endif
         }
-#if RG_TRI_DBG == 3
-        __syncthreads();
-        if (blockIdx.x == 0 && threadIdx.x == 0)
-            for (int i = 0; i < 16; ++i) {
-                const long long z = tri_dbg[0][0];
-                printf("k %d:", 60 + i);
-                for (int w = 0; w < 8; ++w) printf(" [%lld %lld]", tri_dbg[i][2 * w] - z, tri_dbg[i][2 * w + 1] - tri_dbg[i][2 * w]);
-                printf("\n");
-            }
-#endif
-        if (mover) cp_async_wait_all();
+        if (loader) cp_async_wait_all();
         // passes and sweeps: boundary rows handed to CTA 0 and global results
         // must be complete before anyone starts the next one, and the
         // boundary buffers of CTAs >= 1 (fully consumed by now) are armed
@@ -464,7 +427,7 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
 }
 
 template <typename S, int MODE>
-__global__ void __launch_bounds__(2 * TRI_RPC, 1) tri_kernel(const TriArgs<S> a) {
+__global__ void __launch_bounds__(3 * TRI_RPC, 1) tri_kernel(const TriArgs<S> a) {
     extern __shared__ double tri_smem[];
     cg::cluster_group cl = cg::this_cluster();
     TriShared sm;
@@ -517,7 +480,7 @@ cudaError_t launch_tri_m(TriArgs<S> a, int batch, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(batch * a.nc, 1, 1);
-    cfg.blockDim = dim3(2 * TRI_RPC, 1, 1);
+    cfg.blockDim = dim3(3 * TRI_RPC, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
