@@ -218,14 +218,17 @@ int rg_krylov_update(int dtype, int n, void* u, const void* Z, long long ldz, co
                      void* stream);
 
 /* ---- Gauss-Seidel / SOR / SSOR preconditioners (precond.py:79-118) --------
- * z = B^{-1} r for every system of a CONST9 real operator:
+ * z = B^{-1} r for every system of any operator (CONST9 / DIAG5 / VAR9,
+ * real or complex128; constant real stencils take a thread-block-cluster
+ * wavefront, the rest a general one-CTA-per-system wavefront):
  *   RG_TRI_SOR  : z = relax (D + relax L)^{-1} r          (gauss_seidel: relax 1)
  *   RG_TRI_SSOR : z = c (D + relax U)^{-1} D (D + relax L)^{-1} r,
  *                 c = relax (2 - relax)
  * L, U: strict lower / upper parts of A in lexicographic order.  Replaces the
  * SuperLU triangular solves of precond.py:36-45 (agreement to rounding,
  * ~1e-15; the reference's own bar is 1e-13).  relax in (0, 2); a zero
- * diagonal is RG_EINVAL (ZeroDiagonalError).  work: [batch][side*side]
+ * diagonal is RG_EINVAL (ZeroDiagonalError) for CONST9 real operators and
+ * the caller's check otherwise (the coefficients live on the device).  work: [batch][side*side]
  * scratch for SSOR (may be NULL for SOR).  r and z must not alias. */
 enum rg_tri { RG_TRI_SOR = 1, RG_TRI_SSOR = 2,
               /* the transposed maps B^{-T} (Preconditioner.apply_transpose,

@@ -21,6 +21,7 @@
 #include <type_traits>
 #include "cblock.cuh"
 #include "tri.cuh"
+#include "trigen.cuh"
 #include "adjoint.cuh"
 #include "psweep.cuh"
 #include "power.cuh"
@@ -788,25 +789,41 @@ int rg_tri_apply(const rg_op* A, int kind, double relax, const void* r, void* z,
                  void* stream) {
     int rc = check_op(A);
     if (rc) return rc;
-    if (A->d.kind != RG_CONST9 || A->d.dtype == RG_C128)
-        return fail(RG_EUNSUPPORTED, "GS/SOR/SSOR need a CONST9 real operator");
     if (kind < RG_TRI_SOR || kind > RG_TRI_SSOR_T) return fail(RG_EINVAL, "bad triangular kind %d", kind);
     const bool needs_work = kind == RG_TRI_SSOR || kind == RG_TRI_SSOR_T;
     if (!(relax > 0.0 && relax < 2.0)) return fail(RG_EINVAL, "relaxation must be in (0, 2), got %g", relax);
     if (!r || !z || (needs_work && !work)) return fail(RG_ENULL, "null vector");
     if (r == z || work == r || work == z) return fail(RG_EINVAL, "r, z and work must not alias");
-    for (int b = 0; b < (A->d.shared ? 1 : A->d.batch); ++b)
-        if (A->hcoef[(size_t)b * 9 + 4] == 0.0) return fail(RG_EINVAL, "zero diagonal entry in system %d", b);
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
-    if (A->d.dtype == RG_F64) {
-        TriArgs<double> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P, relax,
-                          (const double*)r, (double*)z, (double*)work};
-        e = launch_tri(a, kind, A->d.batch, st);
+    if (A->d.kind == RG_CONST9 && A->d.dtype != RG_C128) {
+        // constant real stencils: the cluster wavefront (tri.cuh)
+        for (int b = 0; b < (A->d.shared ? 1 : A->d.batch); ++b)
+            if (A->hcoef[(size_t)b * 9 + 4] == 0.0) return fail(RG_EINVAL, "zero diagonal entry in system %d", b);
+        if (A->d.dtype == RG_F64) {
+            TriArgs<double> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P, relax,
+                              (const double*)r, (double*)z, (double*)work};
+            e = launch_tri(a, kind, A->d.batch, st);
+        } else {
+            TriArgs<float> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P, relax,
+                             (const float*)r, (float*)z, (float*)work};
+            e = launch_tri(a, kind, A->d.batch, st);
+        }
     } else {
-        TriArgs<float> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P, relax,
-                         (const float*)r, (float*)z, (float*)work};
-        e = launch_tri(a, kind, A->d.batch, st);
+        // per-node coefficients and complex scalars (trigen.cuh); the caller
+        // has checked the diagonal (it lives on the device)
+#define RG_TG(S, C)                                                                               \
+    {                                                                                             \
+        TriGenArgs<S> a{(const C*)A->d.stencil, (const C*)A->d.diag, A->d.shared, A->d.side, A->P, \
+                        relax, (const S*)r, (S*)z, (S*)work};                                     \
+        e = A->d.kind == RG_CONST9 ? launch_trigen<S, K_CONST9>(a, kind, A->d.batch, st)          \
+            : A->d.kind == RG_DIAG5 ? launch_trigen<S, K_DIAG5>(a, kind, A->d.batch, st)          \
+                                    : launch_trigen<S, K_VAR9>(a, kind, A->d.batch, st);          \
+    }
+        if (A->d.dtype == RG_C128) RG_TG(double2, double2)
+        else if (A->d.dtype == RG_F64) RG_TG(double, double)
+        else RG_TG(float, double)
+#undef RG_TG
     }
     return e == cudaSuccess ? RG_OK : fail(RG_ECUDA, "triangular solve launch: %s", cudaGetErrorString(e));
 }

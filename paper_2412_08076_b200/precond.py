@@ -34,7 +34,7 @@ _TRI_KINDS = {"gauss-seidel": L.RG_TRI_SOR, "sor": L.RG_TRI_SOR, "ssor": L.RG_TR
 
 
 class TriangularPreconditioner:
-    """Gauss-Seidel / SOR / SSOR map of one (batched) CONST9 operator."""
+    """Gauss-Seidel / SOR / SSOR map of one (batched) operator."""
 
     def __init__(self, op: GpuStencilOperator, kind: str, relax: float):
         if kind not in _TRI_KINDS:
@@ -44,11 +44,13 @@ class TriangularPreconditioner:
         name = "SSOR" if kind == "ssor" else "SOR"
         if not 0.0 < relax < 2.0:
             raise ValueError(f"{name} relaxation must be in (0, 2), got {relax}")
-        if op.kind != L.RG_CONST9 or op.np_dtype == np.complex128:
-            raise UnsupportedOperator("GS/SOR/SSOR run on constant 9-point real operators")
-        d = np.asarray(op._host_stencil)[:, 4]
-        if np.any(d == 0):
-            raise ZeroDiagonalError(0)
+        # any operator the reference builds these maps for (precond.py:86-118):
+        # constant real stencils take the cluster wavefront (csrc/tri.cuh),
+        # per-node / complex coefficients the general one (csrc/trigen.cuh)
+        for b in range(op.nsets):
+            d = op.diagonal(b)
+            if np.any(d == 0):
+                raise ZeroDiagonalError(int(np.flatnonzero(d == 0)[0]))
         self.op = op
         self.kind = kind
         self.relax = None if kind == "gauss-seidel" else float(relax)
