@@ -438,7 +438,55 @@ def cfg5(ctx):
             "parity": {"rel_vcycle_rhs0": _rel(vg, vo), "bar": 1e-12}}
 
 
-RUNNERS = {"cfg1": cfg1, "cfg2": cfg2, "nag16_sweep": nag16_sweep, "cfg4": cfg4, "cfg5": cfg5}
+def precond_ssor(ctx):
+    """GS/SOR/SSOR application on cfg3's 8 x 1023^2
+    systems: the cluster wavefront of csrc/tri.cuh."""
+    import torch
+    import oracle as O
+    import paper_2412_08076_b200 as G
+    from paper_2412_08076_b200 import configs as CF
+    c = CF.cfg3(first=0, count=8, n=1024, m=32)
+    op = G.GpuStencilOperator.from_problems(c["problems"])
+    B, P, side = op.batch, op.P, op.side
+    R = torch.randn(B, P, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    Z, W = torch.empty_like(R), torch.empty_like(R)
+    out = {}
+    for kind, relax, sweeps in (("sor", 1.5, 1), ("ssor", 1.0, 2)):
+        pre = G.TriangularPreconditioner(op, kind, relax)
+        pre.apply_device(R, Z, W)
+        t = _cuda_time(lambda: pre.apply_device(R, Z, W), reps=10)
+        out[kind] = {"seconds": t, "ns_per_dependent_step": t * 1e9 / (sweeps * (3 * side - 2)),
+                     "point_solves_per_s": sweeps * B * P / t}
+    Rh = R.cpu().numpy()
+    Rp = torch.from_numpy(Rh).pin_memory()
+    pre = G.TriangularPreconditioner(op, "ssor", 1.0)
+    te, Zh = _wall(lambda: pre.apply(Rp))
+    A0 = O.assemble_anisotropic(c["problems"][0].epsilon, c["problems"][0].theta, 1024)
+    f = O.tri_precond(A0, "ssor", 1.0)
+    f(Rh[0])
+    t0 = time.perf_counter()
+    zo = f(Rh[0])
+    tcpu = time.perf_counter() - t0
+    z0 = Zh[0] if not isinstance(Zh, torch.Tensor) else Zh[0].cpu().numpy()
+    return {"workload": "SSOR application z = B^{-1} r, 8 x 1023^2 (cfg3's systems), f64",
+            "metric": "time per application (8 systems)", "value": out["ssor"]["seconds"], "unit": "s",
+            "higher_is_better": False, "sor": out["sor"], "ssor": out["ssor"],
+            "roofline": {"bound": "latency",
+                         "note": "lexicographic substitution: 3 side - 2 = 3067 dependent steps per sweep "
+                                 "(slope-2 wavefront); a bare shuffle + select + 2 DFMA step measures 41 "
+                                 "cycles = 21 ns (profiles/micro/fp64_chain.cu)"},
+            "e2e": {"value": te, "unit": "s", "h2d_bytes_per_step": int(Rh.nbytes),
+                    "d2h_bytes_per_step": int(Rh.nbytes),
+                    "api": "TriangularPreconditioner(op, 'ssor', 1.0).apply(r_pinned_host) -> numpy"},
+            "cpu_baseline": {"value": tcpu, "unit": "s per application per system", "cores": 1,
+                             "kind": "port",
+                             "sample": "1 SSOR application of system 0 (SuperLU triangular solves, "
+                                       "factorisation outside the timing)"},
+            "parity": {"rel_system0": _rel(z0, zo), "bar": 1e-13}}
+
+
+RUNNERS = {"cfg1": cfg1, "cfg2": cfg2, "nag16_sweep": nag16_sweep, "cfg4": cfg4, "cfg5": cfg5,
+           "precond_ssor": precond_ssor}
 
 
 def run_all(root, only=None):
