@@ -1439,16 +1439,16 @@ static int mgs_persist(int batch, int n, S* w, long long ldw, const S* V, long l
     if (!coop || nsm < 1) return -1;
     const int slice = (n + nsm - 1) / nsm;
     const size_t smem = 2 * (size_t)slice * sizeof(S);
-    if (smem + 1024 > (size_t)smem_optin || slice > MGSP_NT * MGSP_R) return -1;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(mgs_persist_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(smem_optin - 1024)) != cudaSuccess)
-            return -1;
-        attr = true;
-    }
+    if (smem + 2048 > (size_t)smem_optin || slice > MGSP_NT * MGSP_R) return -1;   // 1.6 KB static
+    // fewest slice elements per thread that cover the slice (registers)
+    const void* kern = slice <= MGSP_NT * 12 ? (const void*)mgs_persist_kernel<S, 12>
+                       : slice <= MGSP_NT * 14 ? (const void*)mgs_persist_kernel<S, 14>
+                                               : (const void*)mgs_persist_kernel<S, 16>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem_optin - 2048)) !=
+        cudaSuccess)
+        return -1;
     char* ws = nullptr;
-    const size_t part_bytes = sizeof(double) * 3 * 2 * (size_t)nsm;   // two parities
+    const size_t part_bytes = sizeof(double) * MGSP_NV * 2 * (size_t)nsm;   // two parities
     ensure_pool();
     if (cudaMallocAsync((void**)&ws, part_bytes + 2 * sizeof(unsigned int), st) != cudaSuccess) return -1;
     unsigned int* cnt = (unsigned int*)(ws + part_bytes);
@@ -1458,7 +1458,7 @@ static int mgs_persist(int batch, int n, S* w, long long ldw, const S* V, long l
     a.part = (double*)ws; a.bar.count = cnt; a.bar.gen = cnt + 1;
     a.n = n; a.k = k; a.B = batch; a.slice = slice;
     void* args[] = {&a};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)mgs_persist_kernel<S>, dim3(nsm),
+    cudaError_t e = cudaLaunchCooperativeKernel(kern, dim3(nsm),
                                                 dim3(MGSP_NT), args, smem, st);
     cudaFreeAsync(ws, st);
     if (e != cudaSuccess) {        // e.g. co-residency refused: take the multi-launch path

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(MGS_NT) mgs_finish_kernel(const double* part, 
 // grid barrier after which every CTA sums the per-CTA partials in the same
 // fixed order (identical, deterministic h_i in every CTA, no second barrier).
 // Same arithmetic per element as mgs_kernel (w -= h v, conj(v) . w).
-constexpr int MGSP_NT = 512;
+constexpr int MGSP_NT = 512;            // 1024 threads x 7 elements measured slower (0.85 vs 0.77 ms at k = 19)
 
 struct GridBar {
     unsigned int* count;   // arrivals of the current phase
@@ -157,92 +157,214 @@ struct MgsPArgs {
     const S* V; long long ldv;     // basis v_i of system b at V + b*ldv + i*n
     S* H;                          // [k+1][B]
     double* wnorm2;                // [B]
-    double* part;                  // [gridDim][3]
+    double* part;                  // [2][gridDim][MGSP_NV]
     GridBar bar;
     int n, k, B, slice;
 };
 
-constexpr int MGSP_R = 16;          // slice elements per thread (slice <= MGSP_NT * MGSP_R)
+constexpr int MGSP_R = 16;          // most slice elements per thread (slice <= MGSP_NT * MGSP_R); 12 and 14 have instantiations too
+constexpr int MGSP_NV = 6;          // partial sums per CTA and phase
 
+// Sum NV values over the CTA in a fixed order (warp shuffles, one row per
+// warp, the first warp adds the rows); every thread gets the totals.
+template <int NT, int NV>
+__device__ __forceinline__ void block_sum_n(double (&v)[NV], double (*red)[NV], double* out) {
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(0xffffffffu, v[j], o);
+    __syncthreads();                       // red / out of the previous use are free
+    if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) red[wp][j] = v[j];
+    __syncthreads();
+    if (wp == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            double x = lane < NT / 32 ? red[lane][j] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+            if (lane == 0) out[j] = x;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = out[j];
+}
+
+// Fused-multiply-add forms for the Krylov kernels (the library is compiled
+// without contraction for the stencil sums; nothing here is compared
+// bitwise -- the reference's dots go through BLAS): acc + conj(a) b and
+// x - h v.
+__device__ __forceinline__ double2 dot_acc(double2 acc, double2 a, double2 b) {
+    acc.x = fma(a.x, b.x, acc.x); acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y); acc.y = fma(-a.y, b.x, acc.y);
+    return acc;
+}
+__device__ __forceinline__ double dot_acc(double acc, double a, double b) { return fma(a, b, acc); }
+__device__ __forceinline__ double2 sub_mul(double2 x, double2 h, double2 v) {
+    x.x = fma(-h.x, v.x, x.x); x.x = fma(h.y, v.y, x.x);
+    x.y = fma(-h.x, v.y, x.y); x.y = fma(-h.y, v.x, x.y);
+    return x;
+}
+__device__ __forceinline__ double sub_mul(double x, double h, double v) { return fma(-h, v, x); }
+
+// One prefetch.global.L2 per 128-byte line of a CTA's slice.
 template <typename S>
+__device__ __forceinline__ void l2_prefetch_slice(const S* p, int cnt) {
+    constexpr int EPL = 128 / sizeof(S);
+    for (int q = threadIdx.x * EPL; q < cnt; q += MGSP_NT * EPL)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + q));
+}
+
+// The basis vectors are taken two per phase.  For the pair (v_i, v_{i+1})
+// one pass over the slice yields a = <v_i, w>, b = <v_{i+1}, w> and the
+// Gram entry c = <v_{i+1}, v_i>; after the grid barrier
+//     h_i = a,   h_{i+1} = b - h_i c  = <v_{i+1}, w - h_i v_i>
+// which is the modified Gram-Schmidt coefficient itself (fgmres.py:76-78),
+// not the classical one: c is the exact correction (it is ~1e-16 for an
+// orthonormal basis, so the two forms differ far below rounding).  Both
+// projections are then subtracted in MGS order at the start of the next
+// phase, w <- (w - h_i v_i) - h_{i+1} v_{i+1}, with v_i kept in shared
+// memory and v_{i+1} in registers: the number of grid-wide reductions per
+// system drops from k + 2 to ceil((k + 1) / 2) + 1.
+template <typename S, int R_>
 __global__ void __launch_bounds__(MGSP_NT, 1) mgs_persist_kernel(MgsPArgs<S> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     S* ws = reinterpret_cast<S*>(smem_raw);           // [slice] this CTA's w
-    S* vs = ws + a.slice;                              // [slice] this CTA's current v_i
-    __shared__ double red[MGSP_NT / 32];
-    __shared__ double tot[3];
+    S* vs = ws + a.slice;                              // [slice] this CTA's v_i (first of the pair)
+    __shared__ double red[MGSP_NT / 32][MGSP_NV];
+    __shared__ double tot[MGSP_NV];
+    constexpr bool CPLX = sizeof(S) == 16;
     const int j0 = blockIdx.x * a.slice;
     const int cnt = max(0, min(a.n, j0 + a.slice) - j0);
     unsigned int phase = 0;
     if (threadIdx.x == 0) phase = *a.bar.gen;          // barrier phases continue from here
     int par = 0;                                       // partial-sum buffer parity
+    // sum the per-CTA partials of this phase: every CTA adds them in the same
+    // order; the other parity buffer is written next, so one barrier suffices
+    auto reduce_all = [&](double (&v)[MGSP_NV]) {
+        block_sum_n<MGSP_NT, MGSP_NV>(v, red, tot);
+        double* part = a.part + (size_t)par * MGSP_NV * gridDim.x;
+        if (threadIdx.x < MGSP_NV) part[(size_t)blockIdx.x * MGSP_NV + threadIdx.x] = v[threadIdx.x];
+        grid_barrier(a.bar, phase);     // cooperative_groups grid.sync() measured the same
+#pragma unroll
+        for (int j = 0; j < MGSP_NV; ++j) v[j] = 0.0;
+        for (int c = threadIdx.x; c < (int)gridDim.x; c += MGSP_NT)
+#pragma unroll
+            for (int j = 0; j < MGSP_NV; ++j) v[j] += __ldcg(&part[(size_t)c * MGSP_NV + j]);
+        block_sum_n<MGSP_NT, MGSP_NV>(v, red, tot);
+        par ^= 1;
+    };
     for (int b = 0; b < a.B; ++b) {
         S* w = a.w + b * a.ldw + j0;
         const S* Vb = a.V + b * a.ldv + j0;
-        S h = szero<S>();
-        for (int i = 0; i <= a.k + 1; ++i) {
-            const bool last = i == a.k + 1;
-            const S* vn = last ? nullptr : Vb + (size_t)i * a.n;
-            // all of this thread's global loads first (one latency per pass)
-            S vr[MGSP_R], wr[MGSP_R];
+        S hA = szero<S>(), hB = szero<S>();
+        S vrB[R_];
+        bool prevB = false;
+        {
+            S wr[R_];
 #pragma unroll
-            for (int r = 0; r < MGSP_R; ++r) {
+            for (int r = 0; r < R_; ++r) {
                 const int q = threadIdx.x + r * MGSP_NT;
-                if (q < cnt) {
-                    if (!last) vr[r] = vn[q];
-                    if (i == 0) wr[r] = w[q];
-                }
+                if (q < cnt) wr[r] = w[q];
             }
-            S dot = szero<S>();
-            double nn = 0.0;
 #pragma unroll
-            for (int r = 0; r < MGSP_R; ++r) {
+            for (int r = 0; r < R_; ++r) {
                 const int q = threadIdx.x + r * MGSP_NT;
-                if (q < cnt) {
-                    S x = (i == 0) ? wr[r] : ws[q];
-                    if (i > 0) x = sub(x, mul(h, vs[q]));      // w -= h_{i-1} v_{i-1}
-                    ws[q] = x;
-                    if (!last) {
-                        vs[q] = vr[r];
-                        dot = acc_add(dot, conj_mul(vr[r], x));  // <v_i, w>
-                    } else {
-                        nn = sqacc(nn, x);
-                        w[q] = x;                                // w back to global
+                if (q < cnt) ws[q] = wr[r];
+            }
+        }
+        for (int i = 0; i <= a.k; i += 2) {
+            const bool two = i + 1 <= a.k;
+            if (i > 0) {
+#pragma unroll
+                for (int r = 0; r < R_; ++r) {
+                    const int q = threadIdx.x + r * MGSP_NT;
+                    if (q < cnt) {
+                        S x = sub_mul(ws[q], hA, vs[q]);             // w -= h_{i-2} v_{i-2}
+                        if (prevB) x = sub_mul(x, hB, vrB[r]);       // w -= h_{i-1} v_{i-1}
+                        ws[q] = x;
                     }
                 }
             }
-            double re, im = 0.0;
-            if constexpr (sizeof(S) == 16) { re = dot.x; im = dot.y; } else { re = dot; }
-            const double r0 = block_sum<MGSP_NT>(re, red);
-            const double r1 = block_sum<MGSP_NT>(im, red);
-            const double r2 = block_sum<MGSP_NT>(nn, red);
-            double* part = a.part + (size_t)par * 3 * gridDim.x;
-            if (threadIdx.x == 0) {
-                double* p = part + (size_t)blockIdx.x * 3;
-                p[0] = r0; p[1] = r1; p[2] = r2;
+            // v_i -> shared memory (every thread copies and later reads only
+            // its own elements), v_{i+1} -> registers
+            const S* vA = Vb + (size_t)i * a.n;
+            const S* vB = vA + a.n;
+#pragma unroll
+            for (int r = 0; r < R_; ++r) {
+                const int q = threadIdx.x + r * MGSP_NT;
+                if (q < cnt) cp_async_el<sizeof(S)>(&vs[q], &vA[q], true);
             }
-            grid_barrier(a.bar, phase);
-            // every CTA sums the partials in the same order; the other parity
-            // buffer is written next, so no second barrier is needed
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-            for (int c = threadIdx.x; c < (int)gridDim.x; c += MGSP_NT) {
-                s0 += __ldcg(&part[c * 3]); s1 += __ldcg(&part[c * 3 + 1]);
-                s2 += __ldcg(&part[c * 3 + 2]);
+            cp_async_commit();
+            if (two) {
+#pragma unroll
+                for (int r = 0; r < R_; ++r) {
+                    const int q = threadIdx.x + r * MGSP_NT;
+                    if (q < cnt) vrB[r] = vB[q];
+                }
             }
-            s0 = block_sum<MGSP_NT>(s0, red);
-            s1 = block_sum<MGSP_NT>(s1, red);
-            s2 = block_sum<MGSP_NT>(s2, red);
-            if (threadIdx.x == 0) { tot[0] = s0; tot[1] = s1; tot[2] = s2; }
-            __syncthreads();
-            if (!last) {
-                if constexpr (sizeof(S) == 16) h = make_double2(tot[0], tot[1]);
-                else h = tot[0];
-                if (blockIdx.x == 0 && threadIdx.x == 0) a.H[(size_t)i * a.B + b] = h;
-            } else if (blockIdx.x == 0 && threadIdx.x == 0) {
-                a.wnorm2[b] = tot[2];
+            cp_async_wait_all();
+            S dA = szero<S>(), dB = szero<S>(), cc = szero<S>();
+#pragma unroll
+            for (int r = 0; r < R_; ++r) {
+                const int q = threadIdx.x + r * MGSP_NT;
+                if (q < cnt) {
+                    const S x = ws[q], va = vs[q];
+                    dA = dot_acc(dA, va, x);                         // <v_i, w>
+                    if (two) {
+                        dB = dot_acc(dB, vrB[r], x);                 // <v_{i+1}, w>
+                        cc = dot_acc(cc, vrB[r], va);                // <v_{i+1}, v_i>
+                    }
+                }
             }
-            par ^= 1;
+            // next pair (or the next system's w and first pair) towards L2
+            // while this phase's reduction and grid barrier run
+            if (i + 2 <= a.k) {
+                l2_prefetch_slice(vA + 2 * (size_t)a.n, cnt);
+                if (i + 3 <= a.k) l2_prefetch_slice(vA + 3 * (size_t)a.n, cnt);
+            } else if (b + 1 < a.B) {
+                l2_prefetch_slice(a.w + (b + 1) * a.ldw + j0, cnt);
+                l2_prefetch_slice(a.V + (b + 1) * a.ldv + j0, cnt);
+                if (a.k >= 1) l2_prefetch_slice(a.V + (b + 1) * a.ldv + j0 + a.n, cnt);
+            }
+            double v[MGSP_NV];
+            if constexpr (CPLX) {
+                v[0] = dA.x; v[1] = dA.y; v[2] = dB.x; v[3] = dB.y; v[4] = cc.x; v[5] = cc.y;
+            } else {
+                v[0] = dA; v[1] = 0.0; v[2] = dB; v[3] = 0.0; v[4] = cc; v[5] = 0.0;
+            }
+            reduce_all(v);
+            if constexpr (CPLX) {
+                hA = make_double2(v[0], v[1]);
+                hB = sub(make_double2(v[2], v[3]), mul(hA, make_double2(v[4], v[5])));
+            } else {
+                hA = v[0];
+                hB = v[2] - hA * v[4];
+            }
+            prevB = two;
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                a.H[(size_t)i * a.B + b] = hA;
+                if (two) a.H[(size_t)(i + 1) * a.B + b] = hB;
+            }
         }
+        // last projections, ||w||^2, w back to global
+        double nn = 0.0;
+#pragma unroll
+        for (int r = 0; r < R_; ++r) {
+            const int q = threadIdx.x + r * MGSP_NT;
+            if (q < cnt) {
+                S x = sub_mul(ws[q], hA, vs[q]);
+                if (prevB) x = sub_mul(x, hB, vrB[r]);
+                nn = sqacc(nn, x);
+                w[q] = x;
+            }
+        }
+        double v[MGSP_NV] = {nn, 0.0, 0.0, 0.0, 0.0, 0.0};
+        reduce_all(v);
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.wnorm2[b] = v[0];
     }
 }
 
