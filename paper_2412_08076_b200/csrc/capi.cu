@@ -492,6 +492,38 @@ static int sweep_block(const rg_op* A, const rg_sched* s, int k0, int T, bool ja
     return RG_OK;
 }
 
+// The same T plain steps through the wavefront-strip kernel (wave.cuh), no
+// norm epilogue: rg_sweep's smoothing calls (FNS alternations, real V-cycles).
+template <typename S>
+static int sweep_wave(const rg_op* A, const rg_sched* s, int k0, int T, int seg_rows, bool jac_scalar,
+                      const std::vector<double>& hscale, void* uin, void* uout, const void* f,
+                      cudaStream_t st) {
+    static thread_local WaveArgs<S> a;
+    memset(&a.epi, 0, sizeof a.epi);
+    a.side = A->d.side;
+    a.P = A->P;
+    a.u_in = (const S*)uin;
+    a.u_out = (S*)uout;
+    a.f = (const S*)f;
+    a.omega = s->omega;
+    a.m = s->m;
+    a.k0 = k0;
+    a.seg_rows = seg_rows;
+    wave_ntiles(A->d.side, T, seg_rows, &a.nstrip);
+    const int B = A->d.batch;
+    for (int b0 = 0; b0 < B; b0 += BLK_MAXB) {
+        const int nsys = B - b0 < BLK_MAXB ? B - b0 : BLK_MAXB;
+        a.b0 = b0;
+        for (int j = 0; j < nsys; ++j) {
+            for (int d = 0; d < 9; ++d) a.coef[j][d] = A->hcoef[(size_t)(b0 + j) * 9 + d];
+            a.scale[j] = jac_scalar ? hscale[b0 + j] : 0.0;
+        }
+        cudaError_t err = launch_wave<S>(a, T, jac_scalar, nsys, st);
+        if (err != cudaSuccess) return fail(RG_ECUDA, "wave sweep launch: %s", cudaGetErrorString(err));
+    }
+    return RG_OK;
+}
+
 // Length of the blocked chunk that starts at step i of an n-step run: n is
 // split into round(n / T) nearly equal chunks (at most 8 steps each), so a
 // 32-step sweep at T=5 runs as 6,6,5,5,5,5 instead of 5,5,5,5,5,5,2.
@@ -1023,7 +1055,13 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
         CUDA_TRY(cudaMemcpyAsync(hscale.data(), s->scale, B * sizeof(double), cudaMemcpyDeviceToHost, st));
         CUDA_TRY(cudaStreamSynchronize(st));
     }
-    const int T = block_T == 0 ? 5 : block_T;
+    // plain sweeps of enough systems: wavefront strips at depth 4 (as the
+    // solver engine chooses them, rg_solver_create)
+    const int wave_L = (blocked && s->variant == RG_PLAIN && A->d.side >= WV_MIN_SIDE && wave_enabled() &&
+                        block_T == 0)
+                           ? wave_seg_rows(A->d.side, A->d.batch)
+                           : 0;
+    const int T = block_T == 0 ? (wave_L > 0 ? env_int("RG_WAVE_T", 4) : 5) : block_T;
     int k = i0;
     int left = n_steps;
     // automatic depth of the complex blocked sweeps: 4 for the 32-row 5-point
@@ -1131,6 +1169,10 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
                 default: err = launch_cblock<V_NAG>(ca, t, A->d.batch, st); break;
             }
             rc = err == cudaSuccess ? RG_OK : fail(RG_ECUDA, "complex sweep launch: %s", cudaGetErrorString(err));
+        } else if (blocked && wave_L > 0 && t <= WV_TMAX) {
+            rc = A->d.dtype == RG_F64
+                     ? sweep_wave<double>(A, s, k, t, wave_L, jac, hscale, u[cur], u[cur ^ 1], f, st)
+                     : sweep_wave<float>(A, s, k, t, wave_L, jac, hscale, u[cur], u[cur ^ 1], f, st);
         } else if (blocked) {
             rc = A->d.dtype == RG_F64
                      ? sweep_block<double>(A, s, k, t, jac, hscale, u[cur], u[cur ^ 1], v[cur], v[cur ^ 1], f, st)
