@@ -220,3 +220,64 @@ def test_blocked_sweep_deterministic():
         res = G.solve_stationary_batched(op, Fd, wl["schedules"], P, tol=1e-300, max_outer=20)
         for (u, _), r in zip(res, ref):
             assert torch.equal(u, r)
+
+
+def test_cluster_wavefront_deterministic():
+    """The cluster SOR/SSOR wavefront (csrc/tri.cuh): rows handed between CTAs
+    through DSMEM stores over a sentinel and polled by the consumer, and
+    between warps through staged rows ordered by one barrier per window.
+    Sides on both sides of the cluster sizes (1, 2, 5, 8 CTAs, two passes)
+    must return identical bits on every run and match the oracle."""
+    rng = np.random.default_rng(11)
+    for n, B in ((100, 3), (256, 4), (600, 2), (1024, 3), (1100, 1)):
+        A = O.assemble_anisotropic(0.05, 0.7, n)
+        op = G.GpuStencilOperator.from_sparse(A).broadcast(B)
+        R = torch.as_tensor(rng.standard_normal((B, op.P))).cuda()
+        for kind, relax in (("sor", 1.3), ("ssor", 1.1)):
+            pre = G.TriangularPreconditioner(op, kind, relax)
+            ref = pre.apply_device(R).clone()
+            zo = O.tri_precond(A, kind, relax)(R[B - 1].cpu().numpy())
+            got = ref[B - 1].cpu().numpy()
+            assert np.linalg.norm(got - zo) <= 1e-13 * np.linalg.norm(zo), (n, kind)
+            for _ in range(REPEATS):
+                assert torch.equal(pre.apply_device(R), ref), (n, kind)
+
+
+def test_pairwise_mgs_matches_sequential_and_is_deterministic():
+    """rg_mgs_arnoldi (persistent pairwise MGS, csrc/krylov.cuh) against the
+    sequential modified Gram-Schmidt of fgmres.py:76-78 in NumPy, odd and
+    even k, real and complex; identical bits on repeated runs."""
+    from paper_2412_08076_b200 import _lib as L
+    lib = L.load()
+    rng = np.random.default_rng(12)
+    n, mr, B = 255 * 255, 8, 3
+    for tdt, code in ((torch.complex128, L.RG_C128), (torch.float64, L.RG_F64)):
+        Q = rng.standard_normal((B, mr + 1, n))
+        if tdt == torch.complex128:
+            Q = Q + 1j * rng.standard_normal((B, mr + 1, n))
+        # orthonormal bases per system (as the Arnoldi process provides)
+        Qn = np.stack([np.linalg.qr(Q[b].T)[0].T for b in range(B)])
+        V = torch.as_tensor(Qn).to(tdt).cuda().contiguous()
+        w0 = rng.standard_normal((B, n))
+        if tdt == torch.complex128:
+            w0 = w0 + 1j * rng.standard_normal((B, n))
+        for k in (0, 1, 4, 7):
+            outs = []
+            for _ in range(5):
+                w = torch.as_tensor(w0).to(tdt).cuda().contiguous()
+                hb = torch.zeros((mr + 1, B), dtype=tdt, device="cuda")
+                n2 = torch.zeros(B, dtype=torch.float64, device="cuda")
+                L.check(lib.rg_mgs_arnoldi(code, B, n, L.ptr(w), n, L.ptr(V), (mr + 1) * n, k, L.ptr(hb),
+                                           L.ptr(n2), L.stream_ptr()))
+                outs.append((w.clone(), hb.clone(), n2.clone()))
+            for o in outs[1:]:
+                assert all(torch.equal(a, b) for a, b in zip(o, outs[0]))
+            wg, hg, ng = (t.cpu().numpy() for t in outs[0])
+            for b in range(B):
+                wr = w0[b].astype(Qn.dtype).copy()
+                for i in range(k + 1):
+                    h = np.vdot(Qn[b, i], wr)
+                    wr = wr - h * Qn[b, i]
+                    assert abs(hg[i, b] - h) <= 1e-12 * np.linalg.norm(w0[b]), (k, i)
+                assert np.linalg.norm(wg[b] - wr) <= 1e-13 * np.linalg.norm(w0[b])
+                assert abs(ng[b] - np.vdot(wr, wr).real) <= 1e-12 * ng[b]
