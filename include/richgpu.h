@@ -157,6 +157,14 @@ int rg_inner_update(const rg_op* A, const rg_sched* s, int i,
 int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T,
              void* u0, void* u1, void* v0, void* v1, const void* f, int* out_buf,
              void* stream);
+/* rg_sweep whose input v (zero_mask bit 0) and / or u (bit 1) are all zero,
+ * as at the start of every smoothing call (multigrid.py:128 fresh v; :154
+ * zero coarse guess): the caller need not clear u0 / v0, and the blocked
+ * complex sweeps do not read them in their first launch.  zero_mask 0 is
+ * rg_sweep. */
+int rg_sweep_from_zero(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T,
+                       void* u0, void* u1, void* v0, void* v1, const void* f, int zero_mask,
+                       int* out_buf, void* stream);
 
 /* ---- DST-I / FNS correction (transforms.py:24-35, fns.py:30-84) ----------
  * A plan holds the twiddle table and one [batch][side][side] workspace; one

@@ -1026,6 +1026,12 @@ int rg_unroll_adjoint_step_ext(const rg_op* A, const rg_op* At, const rg_sched* 
 
 int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,
              void* u1, void* v0, void* v1, const void* f, int* out_buf, void* stream) {
+    return rg_sweep_from_zero(A, s, i0, n_steps, block_T, u0, u1, v0, v1, f, 0, out_buf, stream);
+}
+
+int rg_sweep_from_zero(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,
+                       void* u1, void* v0, void* v1, const void* f, int zero_mask, int* out_buf,
+                       void* stream) {
     int rc = check_op(A);
     if (rc) return rc;
     if ((rc = check_sched(A, s))) return rc;
@@ -1047,6 +1053,17 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     // sweep is faster, 46 against 71 us)
     const bool cblocked9 = !blocked && A->var9h && s->precond == RG_PRECOND_NONE &&
                            block_T != 1 && (block_T > 1 || A->d.side >= cb9_min_side());
+    // zero_mask: the blocked complex sweeps skip reading an all-zero u / v in
+    // their first launch; every other path gets the zeros written
+    if (zero_mask & ~3) return fail(RG_EINVAL, "bad zero mask %d", zero_mask);
+    int zero_in = zero_mask;
+    if (zero_mask && !((cblocked || cblocked9) && n_steps > 0)) {
+        const size_t bytes = (size_t)A->d.batch * A->P *
+                             (A->d.dtype == RG_C128 ? 16 : (A->d.dtype == RG_F64 ? 8 : 4));
+        if ((zero_mask & 1) && v0) CUDA_TRY(cudaMemsetAsync(v0, 0, bytes, st));
+        if (zero_mask & 2) CUDA_TRY(cudaMemsetAsync(u0, 0, bytes, st));
+        zero_in = 0;
+    }
     std::vector<double> hscale;
     const bool jac = s->precond == RG_PRECOND_JACOBI_SCALAR;
     if (blocked && jac) {
@@ -1138,6 +1155,7 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
             ca.atil = s->alpha_tilde;
             ca.m = s->m;
             ca.k0 = k;
+            ca.zero_in = left == n_steps ? zero_in : 0;
             cudaError_t err;
             switch (s->variant) {
                 case RG_PLAIN: err = launch_cblock9<V_PLAIN>(ca, t, A->d.batch, st); break;
@@ -1162,6 +1180,7 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
             ca.atil = s->alpha_tilde;
             ca.m = s->m;
             ca.k0 = k;
+            ca.zero_in = left == n_steps ? zero_in : 0;
             cudaError_t err;
             switch (s->variant) {
                 case RG_PLAIN: err = launch_cblock<V_PLAIN>(ca, t, A->d.batch, st); break;

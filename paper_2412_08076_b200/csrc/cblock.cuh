@@ -55,6 +55,7 @@ struct CBlockArgs {
     int m;
     int k0;
     int nty;
+    int zero_in;           // bit 0: v_in is all zero, bit 1: u_in is all zero (not read)
 };
 
 __host__ __device__ inline int cblock_ntiles(int side, int T, int* nty) {
@@ -112,8 +113,8 @@ __global__ void __launch_bounds__(CB_NW * 32, CB_MINB) cblock_kernel(const __gri
             const bool in = (gx >= 0) && (gx < side) && (gy >= 0) && (gy < side);
             const int g = in ? gx * side + gy : -1;
             gidx[rr][cc] = g;
-            const C u = in ? a.u_in[base + g] : szero<C>();
-            const C v = (HASV && in) ? a.v_in[base + g] : szero<C>();
+            const C u = (in && !(a.zero_in & 2)) ? a.u_in[base + g] : szero<C>();
+            const C v = (HASV && in && !(a.zero_in & 1)) ? a.v_in[base + g] : szero<C>();
             ur[rr][cc] = u;
             vr[rr][cc] = v;
             sf[r0 + rr][col] = in ? a.f[base + g] : szero<C>();
@@ -276,6 +277,7 @@ struct CBlock9Args {
     int m;
     int k0;
     int nty;
+    int zero_in;                  // as CBlockArgs
 };
 
 template <int VAR, int T>
@@ -315,8 +317,8 @@ __global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __g
             const bool in = (gx >= 0) && (gx < side) && (gy >= 0) && (gy < side);
             const int g = in ? gx * side + gy : -1;
             gidx[rr][cc] = (in && !a.mask[g]) ? -2 - g : g;
-            const C u = in ? a.u_in[base + g] : szero<C>();
-            const C v = (HASV && in) ? a.v_in[base + g] : szero<C>();
+            const C u = (in && !(a.zero_in & 2)) ? a.u_in[base + g] : szero<C>();
+            const C v = (HASV && in && !(a.zero_in & 1)) ? a.v_in[base + g] : szero<C>();
             ur[rr][cc] = u;
             vr[rr][cc] = v;
             sf[r0 + rr][col] = in ? a.f[base + g] : szero<C>();

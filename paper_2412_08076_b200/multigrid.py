@@ -167,22 +167,26 @@ class GpuHierarchy:
             self._ws[(key, k)] = t
         return t
 
-    def _smooth(self, k, f, u, count):
-        """multigrid.py:126-138 on the device; returns the tensor holding u."""
+    def _smooth(self, k, f, u, count, u_zero=False):
+        """multigrid.py:126-138 on the device; returns the tensor holding u.
+        The momentum starts at zero (:128) and, with u_zero, so does the
+        iterate: rg_sweep_from_zero is told instead of clearing the buffers
+        (the fine-level vectors are 67 MB each at 4 x 1023^2 c128)."""
         lvl = self.levels[k]
         if count == 0 or lvl.sched is None:
+            if u_zero:
+                u.zero_()
             return u
         m = lvl.sched.m
         v0, v1 = self._buf("v0", k), self._buf("v1", k)
-        v0.zero_()
         other = self._buf("ua", k) if u.data_ptr() != self._buf("ua", k).data_ptr() else self._buf("ub", k)
         outb = C.c_int()
-        L.check(self.lib.rg_sweep(lvl.op.handle, C.byref(lvl.sched.struct), 0, count * m, 0,
-                                  L.ptr(u), L.ptr(other), L.ptr(v0), L.ptr(v1), L.ptr(f),
-                                  C.byref(outb), L.stream_ptr()))
+        L.check(self.lib.rg_sweep_from_zero(lvl.op.handle, C.byref(lvl.sched.struct), 0, count * m, 0,
+                                            L.ptr(u), L.ptr(other), L.ptr(v0), L.ptr(v1), L.ptr(f),
+                                            1 | (2 if u_zero else 0), C.byref(outb), L.stream_ptr()))
         return u if outb.value == 0 else other
 
-    def _level(self, k, f, u, pre, post):
+    def _level(self, k, f, u, pre, post, u_zero=False):
         lib, s = self.lib, L.stream_ptr()
         if k == self.depth - 1:
             y = self._buf("y", k)
@@ -190,14 +194,13 @@ class GpuHierarchy:
                                        L.ptr(self.coarse_inv), 1, L.ptr(f), L.ptr(y), s))
             return y
         lvl = self.levels[k]
-        u = self._smooth(k, f, u, pre)
+        u = self._smooth(k, f, u, pre, u_zero=u_zero)
         r = self._buf("r", k)
         L.check(lib.rg_residual(lvl.op.handle, L.ptr(u), L.ptr(f), L.ptr(r), None, s))
         fc = self._buf("f", k + 1)
         L.check(lib.rg_restrict(lvl.op.rg_dtype, self.batch, lvl.n, L.ptr(r), L.ptr(fc), s))
-        uc = self._buf("ua", k + 1)
-        uc.zero_()
-        ec = self._level(k + 1, fc, uc, pre, post)
+        uc = self._buf("ua", k + 1)            # zero coarse guess (multigrid.py:154)
+        ec = self._level(k + 1, fc, uc, pre, post, u_zero=True)
         L.check(lib.rg_prolong_add(lvl.op.rg_dtype, self.batch, lvl.n, L.ptr(ec), L.ptr(u), s))
         return self._smooth(k, f, u, post)
 
@@ -205,9 +208,7 @@ class GpuHierarchy:
 
     def _cycle(self, zero_u, pre, post):
         ud = self._buf("ua", 0)
-        if zero_u:
-            ud.zero_()
-        return self._level(0, self._buf("f", 0), ud, pre, post)
+        return self._level(0, self._buf("f", 0), ud, pre, post, u_zero=zero_u)
 
     def apply(self, f, u=None, pre=1, post=1, check=True):
         """One V-cycle on device tensors f, u [batch, P0]; returns a new tensor.
