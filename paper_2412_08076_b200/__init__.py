@@ -21,7 +21,7 @@ from .schedules import (WeightSchedule, chebyshev_schedule, chebyshev_semi_sched
                         stencil_symbol_bounds)
 # the reference's top-level names for the rest of the path (richlab/__init__.py:4-31)
 from .fns import (SpectralCorrection, dst2, dst2_inv, fns_lite_step, sine_basis_eigenvalues,
-                  sine_mode, solve_fns)
+                  sine_mode, solve_fns, solve_fns_batched)
 from .multigrid import (build_hierarchy, prolong, prolongation_matrix, restrict,
                         restriction_matrix, v_cycle)
 from .fgmres import FgmresConfig, fgmres

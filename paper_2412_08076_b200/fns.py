@@ -235,3 +235,50 @@ def solve_fns(A, f, schedule, corr, M, tol=1e-6, max_iters=10_000):
     return (u.cpu().numpy() if host else u.clone()), SolveReport(
         iterations=it, inner_iterations=it * M, converged=converged,
         final_relative_residual=rel, wall_time=time.perf_counter() - t0, trace=np.array(trace))
+
+
+def solve_fns_batched(A, F, schedule, corr, M, tol=1e-6, max_iters=10_000):
+    """fns.py:87-105 for B independent systems at once: A a batched operator,
+    F [B, P], corr one symbol per system (or one shared).  Every system stops
+    on its own (its iterate is frozen at the step that reaches tol, as the
+    reference's loop would leave it) while the rest of the batch goes on.
+    Returns [(u_b, SolveReport_b)]."""
+    t0 = time.perf_counter()
+    op = _op_for(A, F)
+    host = _is_host(F)
+    Ft = op.to_device(F)
+    B = op.batch
+    eng = FnsEngine(op, schedule, corr, M)
+    eng.u[0].zero_()
+    fnorm = torch.linalg.vector_norm(Ft, dim=1).cpu().numpy()
+    rel = np.ones(B)
+    traces = [[1.0] for _ in range(B)]
+    iters = np.zeros(B, dtype=np.int64)
+    done = fnorm == 0.0
+    final = [None] * B
+    for b in np.flatnonzero(done):
+        final[b] = eng.u[0][b].clone()
+    it = 0
+    while not done.all() and it < max_iters:
+        u = eng.step(Ft)
+        it += 1
+        _, n2 = op.residual(u, Ft, want_r=False)
+        r2 = n2.cpu().numpy()
+        for b in np.flatnonzero(~done):
+            if not math.isfinite(r2[b]):
+                raise DivergenceError("hybrid step produced a non-finite iterate", inner_iteration=M)
+            rel[b] = math.sqrt(r2[b]) / fnorm[b]
+            traces[b].append(rel[b])
+            iters[b] = it
+            if rel[b] <= tol:
+                done[b] = True
+                final[b] = u[b].clone()
+    out = []
+    for b in range(B):
+        ub = final[b] if final[b] is not None else eng.u[eng.cur][b]
+        out.append(((ub.cpu().numpy() if host else ub.clone()), SolveReport(
+            iterations=int(iters[b]), inner_iterations=int(iters[b]) * M,
+            converged=bool(done[b]), final_relative_residual=float(rel[b]),
+            wall_time=time.perf_counter() - t0, trace=np.array(traces[b]))))
+    return out
+

@@ -148,3 +148,29 @@ def test_nonfinite_raises():
         GF.solve_fns(A, f, G.WeightSchedule(omega=[1e308, 1e308]), GF.SpectralCorrection(
             np.zeros(A.shape[0]), 16), 4, max_iters=3)
     assert e.value.inner_iteration == 4
+
+
+def test_solve_fns_batched_matches_per_system():
+    """solve_fns_batched: every system follows its own solve_fns (fns.py:87-105)
+    -- same counts, traces and iterates, each stopping on its own; a zero
+    right-hand side converges at once."""
+    rng = np.random.default_rng(21)
+    n, B = 64, 4
+    probs = [(10 ** rng.uniform(-2, 0), rng.uniform(0, np.pi)) for _ in range(B)]
+    As = [O.assemble_anisotropic(e, t, n) for e, t in probs]
+    op = G.GpuStencilOperator.stack([G.GpuStencilOperator.from_sparse(A) for A in As])
+    F = rng.standard_normal((B, As[0].shape[0]))
+    F[3] = 0.0
+    lam = 0.02 * rng.standard_normal((B, As[0].shape[0]))
+    sch = G.WeightSchedule(omega=np.full(4, 0.35))
+    res = GF.solve_fns_batched(op, F, sch, GF.SpectralCorrection(lam, n), 4, tol=0.5, max_iters=30)
+    its = []
+    for b in range(B):
+        u1, r1 = GF.solve_fns(As[b], F[b], sch, GF.SpectralCorrection(lam[b], n), 4, tol=0.5, max_iters=30)
+        ub, rb = res[b]
+        assert rb.iterations == r1.iterations and rb.converged == r1.converged, b
+        assert np.allclose(rb.trace, r1.trace, rtol=1e-12, atol=0)
+        assert np.linalg.norm(ub - u1) <= 1e-12 * max(np.linalg.norm(u1), 1e-300)
+        its.append(rb.iterations)
+    assert its[3] == 0
+
