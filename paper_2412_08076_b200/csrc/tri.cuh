@@ -30,25 +30,31 @@
 // TRI_PF right-hand sides and the TRI_PF look-ahead values of the row above
 // from shared memory, run TRI_PF steps in registers, and store the TRI_PF
 // unscaled results back over the right-hand sides.  Everything else belongs
-// to the mover warps (the second half of the CTA, one per compute warp):
-//   * cp.async of the right-hand sides a few windows ahead (8 lanes per row
-//     segment, coalesced) plus an L2 prefetch further ahead;
-//   * coalesced write-back of the previous window's results, with the output
-//     scale applied on the way;
-//   * the hand-off between CTAs: the mover of a CTA's last warp copies that
-//     warp's last row of the previous window into the boundary buffer of
-//     the next CTA (DSMEM, plain 8-byte stores over a sentinel), and the
-//     mover of the next CTA's first warp polls the columns of the coming
-//     window until they have landed.  No cluster barrier, flag or fence is
-//     on the path (a release store costs a MEMBAR.ALL.GPU that waits for
-//     the warp's outstanding global traffic), and a CTA only ever waits for
-//     its predecessor.
+// to two mover warps per compute warp (a CTA is TRI_RPC compute threads,
+// TRI_RPC write-back threads and TRI_RPC fetch threads):
+//   * fetch warp: cp.async of the right-hand sides TRI_NBUF - 3 windows
+//     ahead (TRI_PF lanes per row segment, coalesced);
+//   * write-back warp: coalesced stores of the previous window's results,
+//     with the output scale applied on the way;
+//   * the hand-off between CTAs: the write-back warp of a CTA's last compute
+//     warp copies that warp's last row of the previous window into the
+//     boundary buffer of the next CTA (DSMEM, plain 8-byte stores over a
+//     sentinel), and the fetch warp of the next CTA's first compute warp
+//     polls the columns of the coming window until they have landed.  No
+//     cluster barrier, flag or fence is on the path (a release store costs
+//     a MEMBAR.ALL.GPU that waits for the warp's outstanding global
+//     traffic), and a CTA only ever waits for its predecessor.
 // Inside a CTA the row above warp w is simply the staged last row of warp
 // w - 1 (windows k - 2 and k - 1, kept alive that long).
 //
-// A system's ~3.3 side dependent steps thus run on up to 8 SMs with 4
-// compute warps each; the single-CTA, barrier-per-step form took 0.80 ms
-// for SOR at 8 x 1023^2 (profiles/ncu_tri_r01.json).
+// A system's ~3.5 side dependent steps thus run on up to 8 SMs with 4
+// compute warps each: SOR at 8 x 1023^2 takes 0.22 ms; the single-CTA,
+// barrier-per-step form took 0.80 ms (profiles/ncu_tri_r01.json).  The
+// CTAs of a system are chained window by window, so the time is (windows
+// of a pass) x (window time of an active CTA): ~1950 cycles per 16-step
+// window against ~700 for the bare recurrence; what is left is the movers'
+// burst after each barrier (the compute warps' first steps of a window run
+// at ~130 cycles while it lasts) and the per-window barrier and loop.
 // Contributions are subtracted with FMAs from rhs/d; SuperLU stores the
 // lower factor pre-divided by the diagonal and substitutes column by
 // column, so results agree to rounding (~1e-15); the reference's own bar
