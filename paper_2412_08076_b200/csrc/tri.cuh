@@ -11,9 +11,9 @@
 // (i, j-1), so the substitution is a slope-2 wavefront: point (i, j) can be
 // computed at step s = j + 2 i.
 //
-// A thread-block cluster of up to 8 CTAs per system.  A pass covers
-// (CTAs x TRI_RPC) grid rows; compute thread t of CTA c owns row
-// p0 + c TRI_RPC + t and walks it left to right one point per step.  Inside
+// A thread-block cluster of up to 8 (16) CTAs per system.  A pass covers
+// (CTAs x RPC) grid rows, RPC = 128 or 64; compute thread t of CTA c owns row
+// p0 + c RPC + t and walks it left to right one point per step.  Inside
 // a warp the rows are skewed by two steps (lane l is at column sigma - 2 l
 // of the warp's local step sigma) and the row above arrives by warp
 // shuffle.  Warps are decoupled: global warp g runs TRI_D = 64 + TRI_PF
@@ -30,8 +30,8 @@
 // TRI_PF right-hand sides and the TRI_PF look-ahead values of the row above
 // from shared memory, run TRI_PF steps in registers, and store the TRI_PF
 // unscaled results back over the right-hand sides.  Everything else belongs
-// to two mover warps per compute warp (a CTA is TRI_RPC compute threads,
-// TRI_RPC write-back threads and TRI_RPC fetch threads):
+// to two mover warps per compute warp (a CTA is RPC compute threads,
+// RPC write-back threads and RPC fetch threads):
 //   * fetch warp: cp.async of the right-hand sides TRI_NBUF - 3 windows
 //     ahead (TRI_PF lanes per row segment, coalesced);
 //   * write-back warp: coalesced stores of the previous window's results,
@@ -47,7 +47,7 @@
 // Inside a CTA the row above warp w is simply the staged last row of warp
 // w - 1 (windows k - 2 and k - 1, kept alive that long).
 //
-// A system's ~3.5 side dependent steps thus run on up to 8 SMs with 4
+// A system's ~3.5 side dependent steps thus run on up to 8 (16) SMs with 4 (2)
 // compute warps each: SOR at 8 x 1023^2 takes 0.22 ms; the single-CTA,
 // barrier-per-step form took 0.80 ms (profiles/ncu_tri_r01.json).  The
 // CTAs of a system are chained window by window, so the time is (windows
@@ -79,9 +79,6 @@ enum { TRI_SOR = 1, TRI_SSOR = 2, TRI_SOR_T = 3, TRI_SSOR_T = 4 };
 #ifndef RG_TRI_PF
 #define RG_TRI_PF 16
 #endif
-#ifndef RG_TRI_RPC
-#define RG_TRI_RPC 128
-#endif
 #ifndef RG_TRI_L2PF
 #define RG_TRI_L2PF 0                   // windows of L2 prefetch distance beyond the cp.async depth (0: none; measured no gain)
 #endif
@@ -93,9 +90,10 @@ constexpr int TRI_AHEAD = TRI_NBUF - 3; // a buffer is refilled two windows afte
 constexpr int TRI_PF = RG_TRI_PF;       // steps per window (8 or 16)
 constexpr int TRI_WS = TRI_PF + 2;      // staged row stride: 16-byte aligned rows, conflict-free 128-bit access
 constexpr int TRI_D = 64 + TRI_PF;      // steps a warp lags its predecessor
-constexpr int TRI_RPC = RG_TRI_RPC;     // rows (compute threads) per CTA
-constexpr int TRI_NCW = TRI_RPC / 32;   // compute warps per CTA (+ as many movers)
-constexpr int TRI_MAXC = 8;             // CTAs per cluster (portable limit)
+// rows (compute threads) per CTA are a template parameter RPC: 128 (clusters
+// of up to 8 CTAs) or 64 (up to 16 CTAs, the non-portable cluster size: half
+// the movers' burst per SM; chosen when the device can hold all the batch's
+// clusters at once, cudaOccupancyMaxActiveClusters)
 static_assert(TRI_NBUF >= 4 && (TRI_NBUF & (TRI_NBUF - 1)) == 0, "staging depth");
 
 template <typename S>
@@ -144,7 +142,7 @@ __device__ __forceinline__ void tri_arm(double* bnd, int side) {
 __device__ __forceinline__ int tri_bnd_idx(int col, int side) { return col ? col - 1 : side - 1; }
 
 struct TriShared {
-    double* stage;   // [TRI_NBUF][TRI_RPC][TRI_WS]: right-hand sides, then unscaled results
+    double* stage;   // [TRI_NBUF][RPC][TRI_WS]: right-hand sides, then unscaled results
     double* bnd;     // [side]: the row above this CTA's first row (previous CTA / previous pass)
 };
 
@@ -154,20 +152,21 @@ struct TriShared {
 // traversal order: l0 (i-1, j-1), l1 (i-1, j), l2 (i-1, j+1), l3 (i, j-1).
 // Windows in which all 32 lanes of a warp are inside the grid run
 // predicate-free.
-template <bool REV, bool MULD, bool SCALE, typename SI, typename SO>
+template <int RPC, bool REV, bool MULD, bool SCALE, typename SI, typename SO>
 __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __restrict__ src,
                                           SO* __restrict__ dst, int side, int P, double oscale,
                                           double l0, double l1, double l2, double l3, double d,
                                           const TriShared& sm, int nc) {
     static_assert(sizeof(SI) == 8 || sizeof(SI) == 4, "element size");
+    constexpr int NCW = RPC / 32;            // compute warps per CTA
     const int crank = (int)cl.block_rank();
     const int lane = threadIdx.x & 31;
-    const int role = threadIdx.x / TRI_RPC;                      // 0 compute, 1 write-back, 2 fetch
+    const int role = threadIdx.x / RPC;                      // 0 compute, 1 write-back, 2 fetch
     const bool mover = role > 0, storer = role == 1, loader = role == 2;
-    const int wp = (threadIdx.x >> 5) - role * TRI_NCW;          // compute warp (owned or served)
+    const int wp = (threadIdx.x >> 5) - role * NCW;          // compute warp (owned or served)
     const int t = wp * 32 + lane;                                // row within the CTA
-    const int gw = crank * TRI_NCW + wp;                         // global warp of the pass
-    const int RPP = nc * TRI_RPC;                                // rows per pass
+    const int gw = crank * NCW + wp;                         // global warp of the pass
+    const int RPP = nc * RPC;                                // rows per pass
     const double rd = 1.0 / d;
     const double m0 = -(l0 * rd), m1 = -(l1 * rd), m2 = -(l2 * rd), m3 = -(l3 * rd);
     const int a0 = TRI_D * gw;              // lane 0 is at column s - a0 at step s
@@ -183,11 +182,11 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
     const long long gs = REV ? -gstride : gstride;
     const int dk = REV ? -TRI_PF : TRI_PF;
     double* stage = sm.stage;
-    auto buf = [&](int k) { return stage + (size_t)(k & (TRI_NBUF - 1)) * TRI_RPC * TRI_WS; };
-    const bool cta_first = wp == 0, cta_last = wp == TRI_NCW - 1;
+    auto buf = [&](int k) { return stage + (size_t)(k & (TRI_NBUF - 1)) * RPC * TRI_WS; };
+    const bool cta_first = wp == 0, cta_last = wp == NCW - 1;
     double* bnd_next = cl.map_shared_rank(sm.bnd, crank + 1 < nc ? crank + 1 : 0);
     for (int p0 = 0; p0 < side; p0 += RPP) {
-        const int row = p0 + crank * TRI_RPC + t;                  // traversal-order grid row
+        const int row = p0 + crank * RPC + t;                  // traversal-order grid row
         const int wrow0 = row - lane;                              // first row of the warp
         const bool row_ok = row < side;
         const int nrows = min(RPP, side - p0);
@@ -432,13 +431,13 @@ __device__ __forceinline__ void tri_sweep(cg::cluster_group& cl, const SI* __res
     }
 }
 
-template <typename S, int MODE>
-__global__ void __launch_bounds__(3 * TRI_RPC, 1) tri_kernel(const TriArgs<S> a) {
+template <typename S, int MODE, int RPC>
+__global__ void __launch_bounds__(3 * RPC, 1) tri_kernel(const TriArgs<S> a) {
     extern __shared__ double tri_smem[];
     cg::cluster_group cl = cg::this_cluster();
     TriShared sm;
-    sm.stage = tri_smem;                                          // [TRI_NBUF][TRI_RPC][TRI_WS]
-    sm.bnd = sm.stage + (size_t)TRI_NBUF * TRI_RPC * TRI_WS;      // [side + 1]
+    sm.stage = tri_smem;                                          // [TRI_NBUF][RPC][TRI_WS]
+    sm.bnd = sm.stage + (size_t)TRI_NBUF * RPC * TRI_WS;      // [side + 1]
     if (a.nc > 1) {
         if (cl.block_rank() > 0) tri_arm(sm.bnd, a.side);
         cl.sync();                                                // armed before any producer store lands
@@ -453,40 +452,45 @@ __global__ void __launch_bounds__(3 * TRI_RPC, 1) tri_kernel(const TriArgs<S> a)
     const size_t base = (size_t)b * a.P;
     if (MODE == TRI_SOR) {
         // relax * solve(r)  (precond.py:93)
-        tri_sweep<false, false, true, S, S>(cl, a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
+        tri_sweep<RPC, false, false, true, S, S>(cl, a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
                                             lo3, d, sm, a.nc);
     } else if (MODE == TRI_SOR_T) {
         // relax * solve_t(r)  (precond.py:94)
-        tri_sweep<true, false, true, S, S>(cl, a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
+        tri_sweep<RPC, true, false, true, S, S>(cl, a.r + base, a.z + base, a.side, a.P, w, lo0, lo1, lo2,
                                            lo3, d, sm, a.nc);
     } else if (MODE == TRI_SSOR_T) {
         // c * dlt(diag * dut(r))  (precond.py:112-113)
         const double cc = w * (2.0 - w);
-        tri_sweep<false, false, false, S, S>(cl, a.r + base, a.work + base, a.side, a.P, 1.0, up0, up1,
+        tri_sweep<RPC, false, false, false, S, S>(cl, a.r + base, a.work + base, a.side, a.P, 1.0, up0, up1,
                                              up2, up3, d, sm, a.nc);
-        tri_sweep<true, true, true, S, S>(cl, a.work + base, a.z + base, a.side, a.P, cc, lo0, lo1, lo2,
+        tri_sweep<RPC, true, true, true, S, S>(cl, a.work + base, a.z + base, a.side, a.P, cc, lo0, lo1, lo2,
                                           lo3, d, sm, a.nc);
     } else {
         // c * du(diag * dl(r))  (precond.py:109-110)
         const double cc = w * (2.0 - w);
-        tri_sweep<false, false, false, S, S>(cl, a.r + base, a.work + base, a.side, a.P, 1.0, lo0, lo1,
+        tri_sweep<RPC, false, false, false, S, S>(cl, a.r + base, a.work + base, a.side, a.P, 1.0, lo0, lo1,
                                              lo2, lo3, d, sm, a.nc);
-        tri_sweep<true, true, true, S, S>(cl, a.work + base, a.z + base, a.side, a.P, cc, up0, up1, up2,
+        tri_sweep<RPC, true, true, true, S, S>(cl, a.work + base, a.z + base, a.side, a.P, cc, up0, up1, up2,
                                           up3, d, sm, a.nc);
     }
 }
 
-template <typename S, int MODE>
-cudaError_t launch_tri_m(TriArgs<S> a, int batch, cudaStream_t st) {
-    a.nc = (a.side + TRI_RPC - 1) / TRI_RPC;
-    if (a.nc > TRI_MAXC) a.nc = TRI_MAXC;
-    const size_t smem = ((size_t)TRI_NBUF * TRI_RPC * TRI_WS + a.side + 1) * sizeof(double);
-    auto k = tri_kernel<S, MODE>;
+template <typename S, int MODE, int RPC>
+cudaError_t launch_tri_r(TriArgs<S> a, int batch, cudaStream_t st, bool probe_only, int* max_clusters) {
+    constexpr int MAXC = RPC == 64 ? 16 : 8;
+    a.nc = (a.side + RPC - 1) / RPC;
+    if (a.nc > MAXC) a.nc = MAXC;
+    const size_t smem = ((size_t)TRI_NBUF * RPC * TRI_WS + a.side + 1) * sizeof(double);
+    auto k = tri_kernel<S, MODE, RPC>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    if (a.nc > 8) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(batch * a.nc, 1, 1);
-    cfg.blockDim = dim3(3 * TRI_RPC, 1, 1);
+    cfg.blockDim = dim3(3 * RPC, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -496,7 +500,25 @@ cudaError_t launch_tri_m(TriArgs<S> a, int batch, cudaStream_t st) {
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (probe_only) return cudaOccupancyMaxActiveClusters(max_clusters, k, &cfg);
     return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+// 64 rows per CTA when every cluster of the batch is resident at once (the
+// chained CTAs of a system then carry half the data movement each: SOR at
+// 1 x 1023^2 219 -> 180 us, 8 x 1023^2 221 -> 213 us, 4 x 2047^2 561 ->
+// 441 us); otherwise 128 rows per CTA, half as many CTAs per system.
+template <typename S, int MODE>
+cudaError_t launch_tri_m(const TriArgs<S>& a, int batch, cudaStream_t st) {
+    static const int force = [] { const char* e = getenv("RG_TRI_RPC"); return e ? atoi(e) : 0; }();
+    if (force != 128 && a.side > 32) {
+        int fit = 0;
+        if (force == 64 ||
+            (launch_tri_r<S, MODE, 64>(a, batch, st, true, &fit) == cudaSuccess && fit >= batch))
+            return launch_tri_r<S, MODE, 64>(a, batch, st, false, nullptr);
+        cudaGetLastError();
+    }
+    return launch_tri_r<S, MODE, 128>(a, batch, st, false, nullptr);
 }
 
 template <typename S>

@@ -226,10 +226,12 @@ def test_cluster_wavefront_deterministic():
     """The cluster SOR/SSOR wavefront (csrc/tri.cuh): rows handed between CTAs
     through DSMEM stores over a sentinel and polled by the consumer, and
     between warps through staged rows ordered by one barrier per window.
-    Sides on both sides of the cluster sizes (1, 2, 5, 8 CTAs, two passes)
+    Sides on both sides of the cluster sizes (2 .. 16 CTAs, two passes), both
+    rows-per-CTA forms,
     must return identical bits on every run and match the oracle."""
     rng = np.random.default_rng(11)
-    for n, B in ((100, 3), (256, 4), (600, 2), (1024, 3), (1100, 1)):
+    # (600, 20): more clusters than the device holds at once -> 128 rows per CTA
+    for n, B in ((100, 3), (256, 4), (600, 2), (1024, 3), (1100, 1), (600, 20)):
         A = O.assemble_anisotropic(0.05, 0.7, n)
         op = G.GpuStencilOperator.from_sparse(A).broadcast(B)
         R = torch.as_tensor(rng.standard_normal((B, op.P))).cuda()
