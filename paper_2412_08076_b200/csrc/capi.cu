@@ -22,6 +22,7 @@
 #include "cblock.cuh"
 #include "tri.cuh"
 #include "trigen.cuh"
+#include "resid.cuh"
 #include "adjoint.cuh"
 #include "psweep.cuh"
 #include "power.cuh"
@@ -710,12 +711,49 @@ int rg_matvec(const rg_op* A, const void* x, void* y, void* stream) {
     return RG_OK;
 }
 
+// r = f - A u (+ per-CTA partials of ||r||^2) for constant real stencils (resid.cuh)
+static int resid9_ncta(const rg_op* A) {
+    return ((A->d.side + RS_TC - 1) / RS_TC) * ((A->d.side + RS_TR - 1) / RS_TR);
+}
+static int launch_resid9(const rg_op* A, const void* u, const void* f, void* r, double* part,
+                         cudaStream_t st) {
+    const dim3 g((A->d.side + RS_TC - 1) / RS_TC, (A->d.side + RS_TR - 1) / RS_TR, A->d.batch);
+    if (A->d.dtype == RG_F64) {
+        ResidArgs<double> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P,
+                            (const double*)u, (const double*)f, (double*)r, part};
+        resid9_kernel<double><<<g, RS_NT, 0, st>>>(a);
+    } else {
+        ResidArgs<float> a{(const double*)A->d.stencil, A->d.shared, A->d.side, A->P,
+                           (const float*)u, (const float*)f, (float*)r, part};
+        resid9_kernel<float><<<g, RS_NT, 0, st>>>(a);
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? RG_OK : fail(RG_ECUDA, "residual launch: %s", cudaGetErrorString(e));
+}
+
 int rg_residual(const rg_op* A, const void* u, const void* f, void* r, double* norm2,
                 void* stream) {
     int rc = check_op(A);
     if (rc) return rc;
     if (!u || !f) return fail(RG_ENULL, "null vector");
     cudaStream_t st = (cudaStream_t)stream;
+    if (A->d.kind == RG_CONST9 && A->d.dtype != RG_C128 && env_int("RG_RESID_TILED", 1)) {
+        // constant real stencils: the shared-memory tiled pass (resid.cuh)
+        const int ncta = resid9_ncta(A);
+        double* part = nullptr;
+        if (norm2) {
+            ensure_pool();
+            CUDA_TRY(cudaMallocAsync((void**)&part, sizeof(double) * ncta * A->d.batch, st));
+        }
+        if ((rc = launch_resid9(A, u, f, r, part, st))) return rc;
+        if (norm2) {
+            sum_partials_kernel<256><<<A->d.batch, 256, 0, st>>>(part, ncta, norm2);
+            const cudaError_t e = cudaGetLastError();
+            CUDA_TRY(cudaFreeAsync(part, st));
+            if (e != cudaSuccess) return fail(RG_ECUDA, "reduce launch: %s", cudaGetErrorString(e));
+        }
+        return RG_OK;
+    }
     StepReq q;
     memset(&q, 0, sizeof q);
     q.u_in = u;
@@ -1373,7 +1411,9 @@ int rg_fns_correct(const rg_op* A, const rg_dst* D, const double* lam, double* u
     cudaStream_t st = (cudaStream_t)stream;
     // r = f - A u (a separate pass: measured faster than recomputing the
     // stencil inside the row transform's load)
-    if (A->d.kind == RG_CONST9 && !A->hcoef.empty()) {
+    if (A->d.kind == RG_CONST9 && env_int("RG_RESID_TILED", 1)) {
+        if ((rc = launch_resid9(A, u, f, D->work, nullptr, st))) return rc;
+    } else if (A->d.kind == RG_CONST9 && !A->hcoef.empty()) {
         if ((rc = resid_const9(A, u, f, D->work, st))) return rc;
     } else {
         StepReq q;
