@@ -280,7 +280,12 @@ struct CBlock9Args {
     int zero_in;                  // as CBlockArgs
 };
 
-template <int VAR, int T>
+// REALC: the repeated stencil c9 has zero imaginary parts (the Galerkin
+// coarsening of the Helmholtz operator away from the sponge: R, P and the
+// interior fine rows are real), so its products take 2 multiplies instead of
+// 4 multiplies + 2 adds, exactly as REALOFF above (equal values, possibly
+// another sign of an exact zero).
+template <int VAR, int T, bool REALC>
 __global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __grid_constant__ CBlock9Args a) {
     typedef double2 C;
     constexpr int LR = CB9_LR, LC = CB9_LC;
@@ -360,15 +365,16 @@ __global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __g
                 const int g = gidx[rr][cc];
                 C s;
                 if (g >= -1) {   // the repeated stencil (or outside the grid)
-                    s = mul(a.c9[0], upw);
-                    s = add(s, mul(a.c9[1], up));
-                    s = add(s, mul(a.c9[2], upe));
-                    s = add(s, mul(a.c9[3], mw));
-                    s = add(s, mul(a.c9[4], mid));
-                    s = add(s, mul(a.c9[5], me));
-                    s = add(s, mul(a.c9[6], dw));
-                    s = add(s, mul(a.c9[7], dn));
-                    s = add(s, mul(a.c9[8], de));
+                    auto pr = [&](int q, const C& x) -> C { return REALC ? rmul(a.c9[q].x, x) : mul(a.c9[q], x); };
+                    s = pr(0, upw);
+                    s = add(s, pr(1, up));
+                    s = add(s, pr(2, upe));
+                    s = add(s, pr(3, mw));
+                    s = add(s, pr(4, mid));
+                    s = add(s, pr(5, me));
+                    s = add(s, pr(6, dw));
+                    s = add(s, pr(7, dn));
+                    s = add(s, pr(8, de));
                 } else {         // band row: its own coefficient planes
                     const C* c = a.planes + (size_t)(-2 - g);
                     s = mul(__ldg(&c[0]), upw);
@@ -414,9 +420,9 @@ __global__ void __launch_bounds__(CB_NW * 32, CB9_MINB) cblock9_kernel(const __g
     }
 }
 
-template <int VAR, int T>
+template <int VAR, int T, bool REALC>
 cudaError_t launch_cblock9_t(const CBlock9Args& a0, int batch, cudaStream_t st) {
-    auto kern = cblock9_kernel<VAR, T>;
+    auto kern = cblock9_kernel<VAR, T, REALC>;
     const size_t smem = 3 * (size_t)CB9_LR * CB9_LC * sizeof(double2);
     static bool attr_set = false;
     if (!attr_set) {
@@ -432,12 +438,18 @@ cudaError_t launch_cblock9_t(const CBlock9Args& a0, int batch, cudaStream_t st) 
 
 template <int VAR>
 cudaError_t launch_cblock9(const CBlock9Args& a, int T, int batch, cudaStream_t st) {
+    bool realc = true;
+    for (int q = 0; q < 9; ++q) realc = realc && a.c9[q].y == 0.0;
+    static const bool allow = [] { const char* e = getenv("RG_CB9_REALC"); return !e || atoi(e) != 0; }();
+    realc = realc && allow;
+#define RG_CB9(TT) return realc ? launch_cblock9_t<VAR, TT, true>(a, batch, st) : launch_cblock9_t<VAR, TT, false>(a, batch, st)
     switch (T) {
-        case 1: return launch_cblock9_t<VAR, 1>(a, batch, st);
-        case 2: return launch_cblock9_t<VAR, 2>(a, batch, st);
-        case 3: return launch_cblock9_t<VAR, 3>(a, batch, st);
-        case 4: return launch_cblock9_t<VAR, 4>(a, batch, st);
+        case 1: RG_CB9(1);
+        case 2: RG_CB9(2);
+        case 3: RG_CB9(3);
+        case 4: RG_CB9(4);
     }
+#undef RG_CB9
     return cudaErrorInvalidValue;
 }
 
