@@ -261,3 +261,33 @@ def test_general_operator_large_and_solve():
                                 max_outer=400)
     assert rep.iterations == ro["iterations"] and rep.converged
     assert _rel(u, uo) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 17, 32, 33, 34, 64, 65, 66, 97, 128, 129, 130, 193, 257])
+def test_apply_small_and_boundary_sizes(n):
+    """Grid sides around every warp / CTA / cluster boundary of the wavefront
+    kernel (1 .. 256 rows: 1 to 4 CTAs of 64 rows, partial warps, one-row
+    grids), SOR / SSOR and the transposed maps, two systems."""
+    rng = np.random.default_rng(100 + n)
+    As = [O.assemble_anisotropic(10 ** rng.uniform(-2, 0), rng.uniform(0, np.pi), n) for _ in range(2)]
+    op = G.GpuStencilOperator.stack([G.GpuStencilOperator.from_sparse(A) for A in As])
+    R = rng.standard_normal((2, As[0].shape[0]))
+    for kind, relax in (("sor", 1.6), ("ssor", 0.9)):
+        P = G.TriangularPreconditioner(op, kind, relax)
+        Z = P.apply(R)
+        Zt = P.apply_transpose(R)
+        for b in range(2):
+            f = O.tri_precond(As[b], kind, relax)
+            assert _rel(Z[b], f(R[b])) <= 1e-13, (n, kind, b)
+            if As[b].shape[0] > 1200:
+                continue
+            # B^{-T} r from dense transposed solves (small grids only)
+            Ad = As[b].toarray()
+            D = np.diag(np.diag(Ad))
+            Lo, Up = np.tril(Ad, -1), np.triu(Ad, 1)
+            if kind == "sor":
+                want = relax * np.linalg.solve((D + relax * Lo).T, R[b])
+            else:
+                c = relax * (2 - relax)
+                want = c * np.linalg.solve((D + relax * Lo).T, D @ np.linalg.solve((D + relax * Up).T, R[b]))
+            assert _rel(Zt[b], want) <= 1e-12, (n, kind, b, "transpose")
