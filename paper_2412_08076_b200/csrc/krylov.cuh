@@ -166,9 +166,11 @@ constexpr int MGSP_R = 16;          // most slice elements per thread (slice <= 
 constexpr int MGSP_NV = 6;          // partial sums per CTA and phase
 
 // Sum NV values over the CTA in a fixed order (warp shuffles, one row per
-// warp, the first warp adds the rows); every thread gets the totals.
+// warp; then NV groups of 32 lanes add the rows, all values at once); every
+// thread gets the totals.
 template <int NT, int NV>
 __device__ __forceinline__ void block_sum_n(double (&v)[NV], double (*red)[NV], double* out) {
+    static_assert(NT / 32 <= 32 && NV * 32 <= NT, "one 32-lane group per value");
     const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
 #pragma unroll
     for (int j = 0; j < NV; ++j)
@@ -179,14 +181,11 @@ __device__ __forceinline__ void block_sum_n(double (&v)[NV], double (*red)[NV], 
 #pragma unroll
         for (int j = 0; j < NV; ++j) red[wp][j] = v[j];
     __syncthreads();
-    if (wp == 0) {
+    if (wp < NV) {                         // warp j adds value j over the NT / 32 rows
+        double x = lane < NT / 32 ? red[lane][wp] : 0.0;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            double x = lane < NT / 32 ? red[lane][j] : 0.0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-            if (lane == 0) out[j] = x;
-        }
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+        if (lane == 0) out[wp] = x;
     }
     __syncthreads();
 #pragma unroll
