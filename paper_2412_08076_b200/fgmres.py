@@ -100,7 +100,7 @@ def _hierarchy_nocheck(precond):
     owner = getattr(precond, "__self__", None)
     if owner is not None and getattr(precond, "__name__", "") == "apply" and \
             type(owner).__name__ == "GpuHierarchy":
-        return lambda R: owner.apply(R, check=False), True
+        return lambda R: owner.apply(R, check=False, clone=False), True
     return precond, False
 
 

@@ -210,7 +210,7 @@ class GpuHierarchy:
         ud = self._buf("ua", 0)
         return self._level(0, self._buf("f", 0), ud, pre, post, u_zero=zero_u)
 
-    def apply(self, f, u=None, pre=1, post=1, check=True):
+    def apply(self, f, u=None, pre=1, post=1, check=True, clone=True):
         """One V-cycle on device tensors f, u [batch, P0]; returns a new tensor.
         check=False skips the host-synchronising non-finite test of
         multigrid.py:135-137 (callers that test later, e.g. the pipelined
@@ -242,7 +242,9 @@ class GpuHierarchy:
             g.replay()
         else:
             out = self._cycle(u is None, pre, post)
-        res = out.clone()
+        # clone=False hands out the hierarchy's own buffer, valid until the next
+        # apply (the FGMRES driver consumes it at once: matvec, store into Z)
+        res = out.clone() if clone else out
         if check and not bool(torch.isfinite(res).all()):
             m = self.levels[0].sched.m if self.levels[0].sched is not None else 0
             raise DivergenceError("smoother produced a non-finite iterate",
