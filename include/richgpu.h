@@ -165,6 +165,15 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
 int rg_sweep_from_zero(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T,
                        void* u0, void* u1, void* v0, void* v1, const void* f, int zero_mask,
                        int* out_buf, void* stream);
+/* rg_sweep that also returns norm2_first[b] = ||f - A u0_b||^2, the residual
+ * norm of the INPUT iterate (device [batch]): the first step computes that
+ * residual anyway, so on the wavefront path the norm rides on the sweep's
+ * fused reduction (fns.py:99 -- the relative residual after a correction is
+ * the first residual of the next alternation's smoothing); other paths take
+ * one rg_residual pass first. */
+int rg_sweep_norm(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T,
+                  void* u0, void* u1, void* v0, void* v1, const void* f,
+                  double* norm2_first, int* out_buf, void* stream);
 
 /* ---- DST-I / FNS correction (transforms.py:24-35, fns.py:30-84) ----------
  * A plan holds the twiddle table and one [batch][side][side] workspace; one

@@ -65,6 +65,7 @@ _SIGS = [
     ("rg_precond_update", _I, [_P, C.POINTER(rg_sched), _I, _P, _P, _P, _P, _P]),
     ("rg_sweep", _I, [_P, C.POINTER(rg_sched), _I, _I, _I, _P, _P, _P, _P, _P, C.POINTER(_I), _P]),
     ("rg_sweep_from_zero", _I, [_P, C.POINTER(rg_sched), _I, _I, _I, _P, _P, _P, _P, _P, _I, C.POINTER(_I), _P]),
+    ("rg_sweep_norm", _I, [_P, C.POINTER(rg_sched), _I, _I, _I, _P, _P, _P, _P, _P, _P, C.POINTER(_I), _P]),
     ("rg_dst_create", _I, [C.POINTER(_P), _I, _I]),
     ("rg_dst_destroy", _I, [_P]),
     ("rg_dst2", _I, [_P, _P, _P, _P]),

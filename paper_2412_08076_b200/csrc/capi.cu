@@ -498,9 +498,10 @@ static int sweep_block(const rg_op* A, const rg_sched* s, int k0, int T, bool ja
 template <typename S>
 static int sweep_wave(const rg_op* A, const rg_sched* s, int k0, int T, int seg_rows, bool jac_scalar,
                       const std::vector<double>& hscale, void* uin, void* uout, const void* f,
-                      cudaStream_t st) {
+                      cudaStream_t st, const EpiArgs* epi = nullptr) {
     static thread_local WaveArgs<S> a;
-    memset(&a.epi, 0, sizeof a.epi);
+    if (epi) a.epi = *epi;
+    else a.epi = EpiArgs{};
     a.side = A->d.side;
     a.P = A->P;
     a.u_in = (const S*)uin;
@@ -1067,9 +1068,26 @@ int rg_sweep(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T
     return rg_sweep_from_zero(A, s, i0, n_steps, block_T, u0, u1, v0, v1, f, 0, out_buf, stream);
 }
 
+static int sweep_impl(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,
+                      void* u1, void* v0, void* v1, const void* f, int zero_mask, double* norm2_first,
+                      int* out_buf, void* stream);
+
 int rg_sweep_from_zero(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,
                        void* u1, void* v0, void* v1, const void* f, int zero_mask, int* out_buf,
                        void* stream) {
+    return sweep_impl(A, s, i0, n_steps, block_T, u0, u1, v0, v1, f, zero_mask, nullptr, out_buf, stream);
+}
+
+int rg_sweep_norm(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,
+                  void* u1, void* v0, void* v1, const void* f, double* norm2_first, int* out_buf,
+                  void* stream) {
+    if (!norm2_first) return fail(RG_ENULL, "null norm output");
+    return sweep_impl(A, s, i0, n_steps, block_T, u0, u1, v0, v1, f, 0, norm2_first, out_buf, stream);
+}
+
+static int sweep_impl(const rg_op* A, const rg_sched* s, int i0, int n_steps, int block_T, void* u0,
+                      void* u1, void* v0, void* v1, const void* f, int zero_mask, double* norm2_first,
+                      int* out_buf, void* stream) {
     int rc = check_op(A);
     if (rc) return rc;
     if ((rc = check_sched(A, s))) return rc;
@@ -1117,6 +1135,14 @@ int rg_sweep_from_zero(const rg_op* A, const rg_sched* s, int i0, int n_steps, i
                            ? wave_seg_rows(A->d.side, A->d.batch)
                            : 0;
     const int T = block_T == 0 ? (wave_L > 0 ? env_int("RG_WAVE_T", 4) : 5) : block_T;
+    // ||f - A u0||^2 per system: the first wavefront launch computes that
+    // residual anyway and reduces its norm in the fused epilogue (stateless
+    // mode); every other path takes a residual pass first
+    const bool norm_fused = norm2_first && wave_L > 0 && n_steps > 0 && A->d.dtype == RG_F64 &&
+                            chunk_len(n_steps, T, 0) <= WV_TMAX;
+    if (norm2_first && !norm_fused) {
+        if ((rc = rg_residual(A, u0, f, nullptr, norm2_first, stream))) return rc;
+    }
     int k = i0;
     int left = n_steps;
     // automatic depth of the complex blocked sweeps: 4 for the 32-row 5-point
@@ -1227,9 +1253,27 @@ int rg_sweep_from_zero(const rg_op* A, const rg_sched* s, int i0, int n_steps, i
             }
             rc = err == cudaSuccess ? RG_OK : fail(RG_ECUDA, "complex sweep launch: %s", cudaGetErrorString(err));
         } else if (blocked && wave_L > 0 && t <= WV_TMAX) {
-            rc = A->d.dtype == RG_F64
-                     ? sweep_wave<double>(A, s, k, t, wave_L, jac, hscale, u[cur], u[cur ^ 1], f, st)
-                     : sweep_wave<float>(A, s, k, t, wave_L, jac, hscale, u[cur], u[cur ^ 1], f, st);
+            if (norm_fused && left == n_steps) {
+                const int ncta = wave_ntiles(A->d.side, t, wave_L, nullptr);
+                const int B = A->d.batch;
+                char* ws = nullptr;
+                const size_t pbytes = sizeof(double) * (size_t)B * NSLOT * ncta;
+                ensure_pool();
+                CUDA_TRY(cudaMallocAsync((void**)&ws, pbytes + sizeof(int) * B, st));
+                CUDA_TRY(cudaMemsetAsync(ws + pbytes, 0, sizeof(int) * B, st));
+                EpiArgs e = {};
+                e.partials = (double*)ws;
+                e.ncta_cap = ncta;
+                e.nslots = 1;
+                e.counters = (int*)(ws + pbytes);
+                e.norm_out = norm2_first;
+                rc = sweep_wave<double>(A, s, k, t, wave_L, jac, hscale, u[cur], u[cur ^ 1], f, st, &e);
+                CUDA_TRY(cudaFreeAsync(ws, st));
+            } else {
+                rc = A->d.dtype == RG_F64
+                         ? sweep_wave<double>(A, s, k, t, wave_L, jac, hscale, u[cur], u[cur ^ 1], f, st)
+                         : sweep_wave<float>(A, s, k, t, wave_L, jac, hscale, u[cur], u[cur ^ 1], f, st);
+            }
         } else if (blocked) {
             rc = A->d.dtype == RG_F64
                      ? sweep_block<double>(A, s, k, t, jac, hscale, u[cur], u[cur ^ 1], v[cur], v[cur ^ 1], f, st)
@@ -1756,7 +1800,7 @@ int rg_solver_destroy(rg_solver* S) {
 }
 
 static EpiArgs solver_epi(rg_solver* S, int j0, int nslots, int with_f) {
-    EpiArgs e;
+    EpiArgs e = {};
     e.st = S->d_st;
     e.trace = S->d_trace;
     e.trace_stride = S->trace_stride;

@@ -43,6 +43,10 @@ struct EpiArgs {
     int nslots;          // residual-norm slots this launch produces
     int with_f;          // slot NSLOT-1 carries ||f||^2 (solver begin)
     int buf;             // ping-pong index of the launch's input iterate
+    // stateless mode (st == null; rg_sweep_norm): the totals of the nslots
+    // slots go to norm_out[b][nslots], tickets come from counters[b]
+    int* counters = nullptr;
+    double* norm_out = nullptr;
 };
 
 // richardson.py:96-136 for the norms j0 .. j0+n-1 (thread 0 of the last CTA).
@@ -114,7 +118,7 @@ __device__ void epilogue(const EpiArgs& e, int b, int cta, int ncta,
     // only thread 0 wrote partials: it alone fences before taking a ticket
     if (tid == 0) {
         __threadfence();
-        const int t = atomicAdd(&e.st[b].counter, 1);
+        const int t = atomicAdd(e.st ? &e.st[b].counter : &e.counters[b], 1);
         is_last = (t == ncta - 1);
         if (is_last) __threadfence();
     }
@@ -130,9 +134,14 @@ __device__ void epilogue(const EpiArgs& e, int b, int cta, int ncta,
         if (tid == 0) tot[q] = s;
     }
     if (tid == 0) {
-        finalize(e.st[b], e.trace + (size_t)b * e.trace_stride, e.cfg, e.j0, e.nslots,
-                 tot, e.with_f, tot[NSLOT - 1], e.buf);
-        e.st[b].counter = 0;
+        if (e.st) {
+            finalize(e.st[b], e.trace + (size_t)b * e.trace_stride, e.cfg, e.j0, e.nslots,
+                     tot, e.with_f, tot[NSLOT - 1], e.buf);
+            e.st[b].counter = 0;
+        } else {
+            for (int q = 0; q < e.nslots; ++q) e.norm_out[(size_t)b * e.nslots + q] = tot[q];
+            e.counters[b] = 0;
+        }
         __threadfence();
     }
 }

@@ -175,19 +175,71 @@ class FnsEngine:
         self.u = [torch.empty((op.batch, op.P), dtype=torch.float64, device=op.device)
                   for _ in range(2)]
         self.cur = 0
+        self.norm2 = torch.empty(op.batch, dtype=torch.float64, device=op.device)
 
-    def step(self, f):
-        """fns_lite_step on the device iterate self.u[self.cur] (no host sync)."""
+    def _third(self):
+        if len(self.u) < 3:
+            self.u.append(torch.empty_like(self.u[0]))
+
+    def step(self, f, want_norm=False, keep_input=False):
+        """fns_lite_step on the device iterate self.u[self.cur] (no host sync).
+
+        want_norm: self.norm2[b] = ||f - A u_b||^2 of the INPUT iterate -- the
+        residual the first smoothing step computes anyway, reduced in that
+        sweep's epilogue (rg_sweep_norm): the relative residual fns.py:99
+        takes after a correction costs no pass of its own, it arrives with
+        the next alternation.  keep_input: the input iterate survives in its
+        buffer (a third buffer takes the ping-pong), so a caller that finds
+        it converged can still return it; self.prev is its index."""
         lib = self.op._lib
         outb = C.c_int()
-        if self.M > 0:
-            L.check(lib.rg_sweep(self.op.handle, C.byref(self.sched.struct), 0, self.M, 0,
-                                 L.ptr(self.u[self.cur]), L.ptr(self.u[self.cur ^ 1]), None, None,
-                                 L.ptr(f), C.byref(outb), L.stream_ptr()))
-            self.cur = self.cur ^ outb.value
-        L.check(lib.rg_fns_correct(self.op.handle, self.plan.h, L.ptr(self.lam),
-                                   L.ptr(self.u[self.cur]), L.ptr(f), L.stream_ptr()))
-        return self.u[self.cur]
+        h, sched, s = self.op.handle, C.byref(self.sched.struct), L.stream_ptr()
+        M, cur = self.M, self.cur
+        self.prev = cur
+        def sweep(i0, n, src, dst, norm):
+            """n smoothing steps from weight index i0, ping-pong src <-> dst;
+            returns the index holding the result."""
+            if norm:
+                L.check(lib.rg_sweep_norm(h, sched, i0, n, 0, L.ptr(self.u[src]), L.ptr(self.u[dst]),
+                                          None, None, L.ptr(f), L.ptr(self.norm2), C.byref(outb), s))
+            else:
+                L.check(lib.rg_sweep(h, sched, i0, n, 0, L.ptr(self.u[src]), L.ptr(self.u[dst]), None,
+                                     None, L.ptr(f), C.byref(outb), s))
+            return src if outb.value == 0 else dst
+
+        if M > 0 and keep_input:
+            self._third()
+            a, b = [i for i in range(3) if i != cur]
+            # constant real stencils on grids of side >= 128 take blocked sweeps:
+            # 4 steps are exactly one launch (cur -> a), the rest runs a <-> b
+            if self.op.kind == L.RG_CONST9 and self.op.side >= 128:
+                first = min(4, M)
+                got = sweep(0, first, cur, a, want_norm)
+                if got != a:
+                    raise RuntimeError("blocked sweep expected to take one launch")
+                cur = a if M == first else sweep(first, M - first, a, b, False)
+            else:        # any other path: work on a copy
+                self.u[a].copy_(self.u[cur])
+                cur = sweep(0, M, a, b, want_norm)
+        elif M > 0:
+            cur = sweep(0, M, cur, (cur + 1) % len(self.u), want_norm)
+        else:
+            if want_norm:
+                L.check(lib.rg_residual(h, L.ptr(self.u[cur]), L.ptr(f), None, L.ptr(self.norm2), s))
+            if keep_input:
+                self._third()
+                a = (cur + 1) % 3
+                self.u[a].copy_(self.u[cur])
+                cur = a
+        self.cur = cur
+        L.check(lib.rg_fns_correct(h, self.plan.h, L.ptr(self.lam), L.ptr(self.u[cur]), L.ptr(f), s))
+        return self.u[cur]
+
+    def residual_norm2(self, f):
+        """||f - A u||^2 of the current iterate (one residual pass)."""
+        L.check(self.op._lib.rg_residual(self.op.handle, L.ptr(self.u[self.cur]), L.ptr(f), None,
+                                         L.ptr(self.norm2), L.stream_ptr()))
+        return self.norm2
 
 
 def fns_lite_step(A, f, u, schedule, M, corr: SpectralCorrection):
@@ -206,35 +258,65 @@ def fns_lite_step(A, f, u, schedule, M, corr: SpectralCorrection):
     return out.cpu().numpy() if host else out.clone()
 
 
+def _fns_drive(eng, Ft, fnorm, tol, max_iters, M):
+    """The loop of fns.py:87-105 for the engine's batch, every system stopping
+    on its own.  The relative residual after alternation j is the first
+    residual of alternation j + 1, so it is taken from that sweep's fused
+    reduction (FnsEngine.step(want_norm=True)): alternation j + 1 runs
+    speculatively, on a buffer of its own, and is discarded for a system
+    that turns out to have converged at j; only the last iterate of a run
+    that exhausts max_iters needs a residual pass of its own.
+    Returns (final [B] of tensors or None, iters, rel, traces, done)."""
+    B = eng.op.batch
+    rel = np.ones(B)
+    traces = [[1.0] for _ in range(B)]
+    iters = np.zeros(B, dtype=np.int64)
+    done = np.asarray(fnorm) == 0.0
+    final = [eng.u[eng.cur][b].clone() if done[b] else None for b in range(B)]
+
+    def record(j, r2, src):
+        for b in np.flatnonzero(~done):
+            if not math.isfinite(r2[b]):
+                raise DivergenceError("hybrid step produced a non-finite iterate", inner_iteration=M)
+            rel[b] = math.sqrt(r2[b]) / fnorm[b]
+            traces[b].append(rel[b])
+            iters[b] = j
+            if rel[b] <= tol:
+                done[b] = True
+                final[b] = src[b].clone()
+
+    it = 0
+    while not done.all() and it < max_iters:
+        eng.step(Ft, want_norm=it >= 1, keep_input=it >= 1)
+        if it >= 1:
+            record(it, eng.norm2.cpu().numpy(), eng.u[eng.prev])
+            if done.all():
+                break
+        it += 1
+    if not done.all() and it >= 1:
+        record(it, eng.residual_norm2(Ft).cpu().numpy(), eng.u[eng.cur])
+    return final, iters, rel, traces, done
+
+
 def solve_fns(A, f, schedule, corr, M, tol=1e-6, max_iters=10_000):
     """fns.py:87-105 on the device: hybrid steps from zero until the relative
-    residual (one fused residual-norm per step, host-polled) reaches tol."""
+    residual (fused into the next alternation's first sweep, host-polled)
+    reaches tol."""
     t0 = time.perf_counter()
     op = _op_for(A, f)
+    if op.batch != 1:
+        raise ValueError("solve_fns drives one system; use solve_fns_batched for batches")
     host = _is_host(f)
     ft = op.to_device(f)
     eng = FnsEngine(op, schedule, corr, M)
     eng.u[0].zero_()
-    fn2 = torch.linalg.vector_norm(ft, dim=1)
-    fnorm = float(fn2[0].item()) if op.batch == 1 else fn2.cpu().numpy()
-    if op.batch != 1:
-        raise ValueError("solve_fns drives one system; use FnsEngine for batches")
-    rel, trace, it = 1.0, [1.0], 0
-    converged = fnorm == 0.0
-    while not converged and it < max_iters:
-        u = eng.step(ft)
-        it += 1
-        _, n2 = op.residual(u, ft, want_r=False)
-        r2 = float(n2[0].item())
-        if not math.isfinite(r2):
-            raise DivergenceError("hybrid step produced a non-finite iterate", inner_iteration=M)
-        rel = math.sqrt(r2) / fnorm
-        trace.append(rel)
-        converged = rel <= tol
-    u = eng.u[eng.cur].reshape(-1)
+    fnorm = torch.linalg.vector_norm(ft, dim=1).cpu().numpy()
+    final, iters, rel, traces, done = _fns_drive(eng, ft, fnorm, tol, max_iters, M)
+    u = (final[0] if final[0] is not None else eng.u[eng.cur][0]).reshape(-1)
     return (u.cpu().numpy() if host else u.clone()), SolveReport(
-        iterations=it, inner_iterations=it * M, converged=converged,
-        final_relative_residual=rel, wall_time=time.perf_counter() - t0, trace=np.array(trace))
+        iterations=int(iters[0]), inner_iterations=int(iters[0]) * M, converged=bool(done[0]),
+        final_relative_residual=float(rel[0]), wall_time=time.perf_counter() - t0,
+        trace=np.array(traces[0]))
 
 
 def solve_fns_batched(A, F, schedule, corr, M, tol=1e-6, max_iters=10_000):
@@ -247,38 +329,15 @@ def solve_fns_batched(A, F, schedule, corr, M, tol=1e-6, max_iters=10_000):
     op = _op_for(A, F)
     host = _is_host(F)
     Ft = op.to_device(F)
-    B = op.batch
     eng = FnsEngine(op, schedule, corr, M)
     eng.u[0].zero_()
     fnorm = torch.linalg.vector_norm(Ft, dim=1).cpu().numpy()
-    rel = np.ones(B)
-    traces = [[1.0] for _ in range(B)]
-    iters = np.zeros(B, dtype=np.int64)
-    done = fnorm == 0.0
-    final = [None] * B
-    for b in np.flatnonzero(done):
-        final[b] = eng.u[0][b].clone()
-    it = 0
-    while not done.all() and it < max_iters:
-        u = eng.step(Ft)
-        it += 1
-        _, n2 = op.residual(u, Ft, want_r=False)
-        r2 = n2.cpu().numpy()
-        for b in np.flatnonzero(~done):
-            if not math.isfinite(r2[b]):
-                raise DivergenceError("hybrid step produced a non-finite iterate", inner_iteration=M)
-            rel[b] = math.sqrt(r2[b]) / fnorm[b]
-            traces[b].append(rel[b])
-            iters[b] = it
-            if rel[b] <= tol:
-                done[b] = True
-                final[b] = u[b].clone()
+    final, iters, rel, traces, done = _fns_drive(eng, Ft, fnorm, tol, max_iters, M)
     out = []
-    for b in range(B):
+    for b in range(op.batch):
         ub = final[b] if final[b] is not None else eng.u[eng.cur][b]
         out.append(((ub.cpu().numpy() if host else ub.clone()), SolveReport(
             iterations=int(iters[b]), inner_iterations=int(iters[b]) * M,
             converged=bool(done[b]), final_relative_residual=float(rel[b]),
             wall_time=time.perf_counter() - t0, trace=np.array(traces[b]))))
     return out
-

@@ -174,3 +174,36 @@ def test_solve_fns_batched_matches_per_system():
         its.append(rb.iterations)
     assert its[3] == 0
 
+
+def test_sweep_norm_is_the_input_residual_norm():
+    """rg_sweep_norm: the norm the first smoothing step reduces in its fused
+    epilogue is ||f - A u0||^2 of the input iterate (fns.py:99 after a
+    correction), on the wavefront path (8 systems at 255^2) and on the
+    fallback paths (one system; a small grid), and the sweep itself is the
+    plain rg_sweep (bitwise)."""
+    import ctypes as C
+    from paper_2412_08076_b200 import _lib as L
+    from paper_2412_08076_b200.richardson import DeviceSchedule
+    rng = np.random.default_rng(31)
+    for n, B in ((256, 8), (256, 1), (48, 3)):
+        As = [O.assemble_anisotropic(10 ** rng.uniform(-2, 0), rng.uniform(0, np.pi), n) for _ in range(B)]
+        op = G.GpuStencilOperator.stack([G.GpuStencilOperator.from_sparse(A) for A in As])
+        sch = DeviceSchedule(op, G.WeightSchedule(omega=np.full(8, 0.3)), None)
+        U0 = torch.as_tensor(rng.standard_normal((B, op.P))).cuda()
+        F = torch.as_tensor(rng.standard_normal((B, op.P))).cuda()
+        outs = []
+        for with_norm in (False, True):
+            u0, u1 = U0.clone(), torch.empty_like(U0)
+            n2 = torch.zeros(B, dtype=torch.float64, device="cuda")
+            ob = C.c_int()
+            if with_norm:
+                L.check(op._lib.rg_sweep_norm(op.handle, C.byref(sch.struct), 0, 8, 0, L.ptr(u0), L.ptr(u1),
+                                              None, None, L.ptr(F), L.ptr(n2), C.byref(ob), L.stream_ptr()))
+            else:
+                L.check(op._lib.rg_sweep(op.handle, C.byref(sch.struct), 0, 8, 0, L.ptr(u0), L.ptr(u1),
+                                         None, None, L.ptr(F), C.byref(ob), L.stream_ptr()))
+            outs.append(((u0, u1)[ob.value].clone(), n2.cpu().numpy()))
+        assert torch.equal(outs[0][0], outs[1][0]), (n, B)
+        for b in range(B):
+            want = np.linalg.norm(F[b].cpu().numpy() - As[b] @ U0[b].cpu().numpy()) ** 2
+            assert abs(outs[1][1][b] - want) <= 1e-12 * want, (n, B, b)
