@@ -406,6 +406,7 @@ def cfg5(ctx):
     GG.fgmres_batched(op, Fd, precond_apply=h.apply, cfg=cfg)
     tf, res = _wall(lambda: GG.fgmres_batched(op, Fd, precond_apply=h.apply, cfg=cfg))
     Fh = torch.from_numpy(F).pin_memory()
+    GG.fgmres_batched(op, Fh, precond_apply=h.apply, cfg=cfg)     # host-buffer path warm (allocator)
     te, res_e = _wall(lambda: GG.fgmres_batched(op, Fh, precond_apply=h.apply, cfg=cfg))
     steps = max(r.iterations for _, r in res)
     m = len(s.omega)
