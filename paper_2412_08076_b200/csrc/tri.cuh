@@ -559,4 +559,8 @@ __global__ void pupdate_kernel(int B, int P, const S* z, S* u, S* v, S* y, const
     }
 }
 
+// instantiated in tri.cu (parallel build)
+extern template cudaError_t launch_tri<double>(const TriArgs<double>&, int, int, cudaStream_t);
+extern template cudaError_t launch_tri<float>(const TriArgs<float>&, int, int, cudaStream_t);
+
 }  // namespace rg

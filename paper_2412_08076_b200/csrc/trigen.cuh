@@ -189,4 +189,14 @@ cudaError_t launch_trigen(const TriGenArgs<S>& a, int mode, int batch, cudaStrea
 #undef RG_TG
 }
 
+// instantiated in trigen.cu (parallel build)
+#define RG_TRIGEN_EXTERN(S)                                                                              \
+    extern template cudaError_t launch_trigen<S, K_CONST9>(const TriGenArgs<S>&, int, int, cudaStream_t); \
+    extern template cudaError_t launch_trigen<S, K_DIAG5>(const TriGenArgs<S>&, int, int, cudaStream_t);  \
+    extern template cudaError_t launch_trigen<S, K_VAR9>(const TriGenArgs<S>&, int, int, cudaStream_t);
+RG_TRIGEN_EXTERN(float)
+RG_TRIGEN_EXTERN(double)
+RG_TRIGEN_EXTERN(double2)
+#undef RG_TRIGEN_EXTERN
+
 }  // namespace rg
